@@ -1,0 +1,200 @@
+"""Oracle: QTT layout, the truncation rank rule, TT-SVD (Alg. 1 + max-rank
+modification (1)) and Full (Alg. 3).
+
+TEST INFRASTRUCTURE ONLY — see oracle/__init__.py.  Plain numpy float64,
+written to be checked against PAPER.md by eye; no blocking, fusion or
+reordering beyond what Alg. 1 / Alg. 3 state.
+"""
+
+import numpy as np
+
+
+# ---------------------------------------------------------------------------
+# QTT layout (readings Q7, Q8)
+# ---------------------------------------------------------------------------
+
+def axes_descriptor(D, bits, layout):
+    """(axis, bit) for every QTT position p = 1..d (returned 0-based list).
+
+    P:303 fixes 1D: i = sum_k i_k 2^{k-1}, LSB first (reading Q7).
+    leaves the 2D mode order open (reading Q8): 'interleaved' puts x-bit t at
+    position 2t-1 and y-bit t at 2t (x first); 'concat' puts all x-bits, then
+    all y-bits.  `bit` is 1-based, LSB = 1.
+    """
+    if D == 1:
+        return [(0, t) for t in range(1, bits[0] + 1)]
+    bx, by = bits
+    if layout == "interleaved":
+        if bx != by:
+            raise ValueError("interleaved layout needs a square grid")
+        out = []
+        for t in range(1, bx + 1):
+            out.append((0, t))
+            out.append((1, t))
+        return out
+    if layout == "concat":
+        return [(0, t) for t in range(1, bx + 1)] + [(1, t) for t in range(1, by + 1)]
+    raise ValueError(layout)
+
+
+def to_qtt(x, layout="1d"):
+    """Vector v in QTT order: v[sum_p i_p 2^{p-1}] = x at the grid point whose
+    axis bits are the i_p.
+
+    1D / concat: the array in memory (row-major image, x fastest) is already
+    in QTT order.  Interleaved: position 2t-1 is x-bit t, 2t is y-bit t.
+    """
+    x = np.asarray(x)
+    if layout in ("1d", "concat") or x.ndim == 1:
+        return np.ascontiguousarray(x).reshape(-1)
+    ny, nx = x.shape
+    b = int(np.log2(nx))
+    assert nx == ny == 1 << b
+    # image[iy, ix] with iy = sum y_t 2^{t-1}; C-order axes (y_b..y_1, x_b..x_1)
+    t = x.reshape([2] * (2 * b))
+    # QTT index q = x1 + 2 y1 + 4 x2 + ...; as a C-order array its axes are
+    # (y_b, x_b, y_{b-1}, x_{b-1}, ..., y_1, x_1)
+    order = []
+    for k in range(b):          # k = 0 is the most significant bit
+        order.append(k)         # y_{b-k}
+        order.append(b + k)     # x_{b-k}
+    return np.ascontiguousarray(t.transpose(order)).reshape(-1)
+
+
+def from_qtt(v, shape, layout="1d"):
+    """Inverse of to_qtt."""
+    v = np.asarray(v)
+    if layout in ("1d", "concat") or len(shape) == 1:
+        return v.reshape(shape)
+    ny, nx = shape
+    b = int(np.log2(nx))
+    t = v.reshape([2] * (2 * b))          # axes (y_b, x_b, ..., y_1, x_1)
+    inv = [2 * k for k in range(b)] + [2 * k + 1 for k in range(b)]
+    return np.ascontiguousarray(t.transpose(inv)).reshape(shape)
+
+
+# ---------------------------------------------------------------------------
+# Rank rule: eps-rank + max-rank modification (1)
+# + cluster rule (reading Q6 / SURVEY §8(c) O1 RANK)
+# ---------------------------------------------------------------------------
+
+def rank_rule(lam, tau2, rmax, cluster_tol):
+    """RANK(lambda, tau^2, R, delta_c).
+
+    lam: squared singular values, descending.  T(r) = sum_{i>r} lam_i is
+    accumulated from the smallest value up.  r_tau = min{r >= 1 : T(r) <=
+    tau^2} is rank_tau of P:286 (inclusive <=, reading Q2); r = min(r_tau, R)
+    is modification (1) (reading Q3).  A cut inside a cluster of
+    (numerically) equal values, lam_r - lam_{r+1} <= delta_c lam_r, is moved
+    up to the end of the cluster when the tolerance allows it and the cap
+    still holds, else down to its start (reading Q6; the gap is relative to
+    lam_r, not lam_1 — with lam_1 every value below sqrt(delta_c) sigma_1 is
+    one "cluster" and the paper's ranks 17/26 come out full,
+    DESIGN.md §3 reading Q6').
+    """
+    lam = np.maximum(np.asarray(lam, dtype=np.float64), 0.0)
+    m = lam.shape[0]
+    if m == 0 or not lam[0] > 0.0:
+        return 1
+    tail = np.zeros(m + 1)                 # tail[r] = T(r), r = 0..m
+    for r in range(m - 1, -1, -1):
+        tail[r] = tail[r + 1] + lam[r]
+    r_tau = m
+    for r in range(1, m + 1):
+        if tail[r] <= tau2:
+            r_tau = r
+            break
+    r = min(r_tau, rmax)
+
+    def cl(q):
+        return q < m and lam[q - 1] > 0.0 and \
+            (lam[q - 1] - lam[q]) <= cluster_tol * lam[q - 1]
+
+    if cl(r):
+        if r_tau <= rmax:
+            rp = r + 1
+            while cl(rp):
+                rp += 1
+            if rp <= rmax:
+                return rp
+        while r > 1 and cl(r):
+            r -= 1
+    return r
+
+
+# ---------------------------------------------------------------------------
+# Alg. 1 TT-SVD with modification (1)
+# ---------------------------------------------------------------------------
+
+def tt_svd(v, eps, rmax, cluster_tol=1e-10, return_info=False):
+    """Max-rank TT-SVD of a 2x...x2 tensor given as its QTT-ordered vector.
+
+    tau = eps ||A||_F / sqrt(d-1) (P:282 with M-1 read as d-1, reading Q1).
+    Step k: A^{k} = reshape(A, [2 r_{k-1}, |A|/(2 r_{k-1})]) (column-major,
+    P:234/P:248), truncated SVD with ||E||_F <= tau and r_k <= R_max,
+    core_k = reshape(U, [r_{k-1}, 2, r_k]), A := Sigma V^* (P:285-288);
+    core_d := A.
+    """
+    v = np.asarray(v, dtype=np.float64).reshape(-1)
+    n = v.shape[0]
+    d = int(round(np.log2(n)))
+    if (1 << d) != n or d < 2:
+        raise ValueError("length must be 2^d with d >= 2")
+    norm2 = float(np.dot(v, v))
+    tau2 = eps * eps * norm2 / (d - 1)
+    cores = []
+    shapes = []
+    r_prev = 1
+    W = v
+    for k in range(1, d):
+        M = np.reshape(W, (2 * r_prev, -1), order="F")
+        shapes.append(M.shape)
+        U, s, Vt = np.linalg.svd(M, full_matrices=False)
+        r = rank_rule(s * s, tau2, rmax, cluster_tol)
+        cores.append(np.reshape(U[:, :r], (r_prev, 2, r), order="F"))
+        W = s[:r, None] * Vt[:r, :]
+        r_prev = r
+    cores.append(np.reshape(W, (r_prev, 2, 1), order="F"))
+    if return_info:
+        return cores, {"unfolding_shapes": shapes, "tau2": tau2, "norm2": norm2}
+    return cores
+
+
+def ranks_of(cores):
+    """r_0 .. r_d."""
+    return [cores[0].shape[0]] + [c.shape[2] for c in cores]
+
+
+def storage_count(cores):
+    """N_el = sum_k r_{k-1} M_k r_k."""
+    return int(sum(c.size for c in cores))
+
+
+# ---------------------------------------------------------------------------
+# Alg. 3 Full and single elements
+# ---------------------------------------------------------------------------
+
+def full(cores):
+    """A = core_1; for k = 2..K: A = reshape(A, [|A|/r_{k-1}, r_{k-1}]) @
+    reshape(core_k, [r_{k-1}, 2 r_k]); return the QTT-ordered vector."""
+    r1 = cores[0].shape[2]
+    A = np.reshape(cores[0], (2, r1), order="F")
+    for k in range(1, len(cores)):
+        c = cores[k]
+        rk_1, _, rk = c.shape
+        A = np.reshape(A, (A.size // rk_1, rk_1), order="F") @ \
+            np.reshape(c, (rk_1, 2 * rk), order="F")
+    return np.reshape(A, (-1,), order="F")
+
+
+def element(cores, q):
+    """a(i_1..i_K) = A^(1)_{i_1} ... A^(K)_{i_K} at QTT indices q
+    (scalar or 1D integer array)."""
+    q = np.atleast_1d(np.asarray(q, dtype=np.int64))
+    out = None
+    for k, c in enumerate(cores):
+        bit = (q >> k) & 1
+        sl = c[:, bit, :]                      # (r0, nq, r1)
+        sl = np.transpose(sl, (1, 0, 2))       # (nq, r0, r1)
+        out = sl if out is None else np.einsum("nab,nbc->nac", out, sl)
+    return out[:, 0, 0]
