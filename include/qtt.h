@@ -1,0 +1,169 @@
+/*
+ * qtt.h — C ABI of libqtt.so: end-to-end QTT convolution on B200 (sm_100a).
+ *
+ * Implements the hot path of arXiv 2301.13339, Alg. 2 "QTT convolution"
+ * (PAPER.md P:384-399):
+ *   Step 1  reshape the full arrays to 2 x ... x 2 tensors
+ *   Step 2  max-rank TT-SVD of signal and kernel                  (Alg. 1,
+ *           P:275-293, modification (1) P:357-358)
+ *   Step 3  QiFFT( QFFT(F) (.) QFFT(G) ) with capped ranks        (P:395,
+ *           P:309-321), TT-rounding after the Hadamard product
+ *   Step 4  Full                                                   (Alg. 3,
+ *           P:408-424)
+ * Readings of passages the paper leaves open are listed in DESIGN.md §3
+ * (Q1-Q29); the same readings are implemented by the CPU oracle (oracle/).
+ *
+ * Conventions shared by every call
+ *   - Pointers are DEVICE pointers unless the name ends in _host.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream).  Calls do not synchronise the
+ *     host unless documented ("syncs").
+ *   - No call allocates device memory: all scratch and all device storage of
+ *     TT handles is carved from the caller's workspace `ws` (>= the size
+ *     returned by qtt_workspace_bytes, 256-byte aligned).  The workspace must
+ *     stay alive and untouched while the handles carved from it are used.
+ *   - Arrays are float64.  1D: x[i], i = 0..2^b-1.  2D: row-major image
+ *     x[iy * 2^bx + ix] (x fastest).  QTT bit order is LSB first;
+ *     the 2D mode order is the `layout` field (reading Q8).
+ *   - Truncation (reading Q1-Q6): per-cut threshold
+ *     tau^2 = eps^2 ||A||_F^2 / (d-1), rank = min(rank_tau, rmax) moved out
+ *     of clusters of relative width cluster_tol (Q6').
+ *   - Errors: argument errors are reported synchronously (QTT_EINVAL).
+ *     Numeric failures (non-finite input, eigensolver non-convergence) are
+ *     latched in a device status word and returned by the next syncing call
+ *     (qtt_wait, qtt_ranks, qtt_conv_full with a report) as QTT_ENUMERIC.
+ *     CUDA errors -> QTT_ECUDA.  No C++ exception crosses the ABI.  The
+ *     message of the last error of the calling thread is qtt_last_error().
+ */
+#ifndef QTT_H
+#define QTT_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  QTT_OK = 0,
+  QTT_EINVAL = 1,    /* bad argument (sizes, caps, layout, workspace)        */
+  QTT_ENUMERIC = 2,  /* non-finite data or eigensolver failure (latched)     */
+  QTT_ECUDA = 3,     /* CUDA runtime error                                   */
+  QTT_ENCCL = 4,     /* collective failure (multi-GPU builds)                */
+  QTT_ENOMEM = 5     /* workspace too small                                  */
+} qtt_status;
+
+typedef enum {
+  QTT_LAYOUT_1D = 0,
+  QTT_LAYOUT_INTERLEAVED = 1,  /* QTT position 2t-1 = x-bit t, 2t = y-bit t  */
+  QTT_LAYOUT_CONCAT = 2        /* all x-bits, then all y-bits                */
+} qtt_layout;
+
+/* Problem shape.  D in {1,2}; bits[0] = bits of x (length 2^bits[0]),
+ * bits[1] = bits of y (2D).  d = bits[0] (+ bits[1]) must lie in [2, 30].
+ * Interleaved needs bits[0] == bits[1].  batch >= 1 independent signals;
+ * f_stride / y_stride: elements between consecutive batch entries
+ * (0 => 2^d); g_stride: 0 = one kernel shared by the whole batch. */
+typedef struct {
+  int D;
+  int bits[2];
+  int layout;
+  int batch;
+  long long f_stride, g_stride, y_stride;
+} qtt_shape;
+
+/* Truncation policy: eps >= 0, 1 <= rmax <= 16, cluster_tol >= 0.
+ * Decomposition caps use rmax (R_max); transform/rounding caps Rhat. */
+typedef struct {
+  double eps;
+  int rmax;
+  double cluster_tol;
+} qtt_trunc;
+
+typedef struct qtt_tt_s* qtt_tt_t;      /* opaque TT tensor (batch of them)  */
+typedef struct qtt_comm_s* qtt_comm_t;  /* NULL = single GPU                 */
+
+/* Optional report of qtt_conv_full (host struct, filled when non-NULL;
+ * filling it syncs the stream).  ranks_*: r_0..r_d of batch entry 0. */
+typedef struct {
+  int d;
+  int ranks_f[64], ranks_g[64], ranks_fh[64], ranks_gh[64], ranks_z[64],
+      ranks_out[64];
+  float ms_total;
+} qtt_report;
+
+/* Bytes of workspace needed by qtt_conv_full (and enough for any single
+ * qtt_decompose / qtt_convolve / qtt_to_full of the same shape and caps).
+ * Returns 0 for invalid arguments.  nranks: 1 (multi-GPU reserved). */
+size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec,
+                           const qtt_trunc* fft, int nranks);
+
+/* Step 1-2: max-rank TT-SVD (Alg. 1 + mod (1)) of the batch of
+ * arrays x (shape->batch of them, stride shape->f_stride).  Writes a new
+ * handle to *out whose device storage lives in ws. */
+qtt_status qtt_decompose(const double* x, const qtt_shape* shape,
+                         const qtt_trunc* dec, void* ws, size_t ws_bytes,
+                         void* stream, qtt_comm_t comm, qtt_tt_t* out);
+
+/* QTT-FFT (inverse = 0) or QTT-iFFT (inverse = 1) of every tensor of `in`
+ * (capped P:370-382).  Forward output is the bit-reversed layout
+ * of SURVEY §8(c) O2; if shift != NULL the forward output is multiplied by
+ * the centering phase of shift (O3); the inverse output is scaled by
+ * scale * 2^{-d}.  Test/diagnostic entry point of the Step-3 machinery. */
+qtt_status qtt_transform(qtt_tt_t in, const qtt_trunc* fft, int inverse,
+                         const long long shift[2], double scale, void* ws,
+                         size_t ws_bytes, void* stream, qtt_tt_t* out);
+
+/* Step 3: QiFFT(round(QFFT(f) (.) center(QFFT(g)))) scaled by
+ * `scale` (= dx^D, eq. dconv).  g holds 1 tensor (shared) or as many
+ * as f.  y_j = scale sum_i f_i g_{(j - i + shift) mod n} per axis. */
+qtt_status qtt_convolve(qtt_tt_t f, qtt_tt_t g, const qtt_trunc* fft,
+                        const long long shift[2], double scale, void* ws,
+                        size_t ws_bytes, void* stream, qtt_tt_t* out);
+
+/* Step 4 (Alg. 3): y = Re(full(t)) written in the caller layout
+ * (batch stride y_stride of t's shape).  If y_imag != NULL the imaginary
+ * part is written there too (diagnostics). */
+qtt_status qtt_to_full(qtt_tt_t t, double* y, double* y_imag, void* ws,
+                       size_t ws_bytes, void* stream, qtt_comm_t comm);
+
+/* Alg. 2 end to end: y = QTT convolution of f and g (Steps 1-4). */
+qtt_status qtt_conv_full(const double* f, const double* g, double* y,
+                         const qtt_shape* shape, const qtt_trunc* dec,
+                         const qtt_trunc* fft, const long long shift[2],
+                         double scale, void* ws, size_t ws_bytes,
+                         void* stream, qtt_comm_t comm,
+                         qtt_report* rep_host);
+
+/* Syncs; returns the latched numeric status of the handle's stream work. */
+qtt_status qtt_wait(qtt_tt_t t);
+/* Syncs; copies r_0..r_d of batch entry `index` into ranks_host (cap >= d+1). */
+qtt_status qtt_ranks(qtt_tt_t t, int index, int* ranks_host, int cap);
+/* Number of modes d of the handle's tensors (host only). */
+int qtt_ndims(qtt_tt_t t);
+/* Releases the host handle (device storage belongs to the workspace). */
+void qtt_destroy(qtt_tt_t t);
+
+/* TEST-ONLY: Hermitian eigendecomposition of the n x n (n <= 32) complex
+ * matrix A (device, column-major interleaved re/im doubles) by the CTA Jacobi
+ * solver every truncation of the path uses.  lam (device, n): eigenvalues in
+ * descending order; U (device, n x n complex): eigenvectors; sweeps (device
+ * int): Jacobi sweeps used.  Stream-ordered, no sync. */
+int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, void* stream);
+
+/* TEST-ONLY: build a handle from host cores (shape->batch tensors; tensor i,
+ * core k occupies the slot of 512 complex starting at ((i*d)+k)*512, compact
+ * column-major (r_{k-1}, 2, r_k); ranks_host: 64 ints per tensor).  Syncs.
+ * Lets a test run one stage of the GPU path on a known input. */
+qtt_status qtt_debug_tt_from_host(const qtt_shape* shape, const void* cores_host,
+                                  const int* ranks_host, int rcap, void* ws,
+                                  size_t ws_bytes, void* stream, qtt_tt_t* out);
+
+const char* qtt_status_string(qtt_status s);
+const char* qtt_last_error(void);   /* thread-local, never NULL */
+const char* qtt_build_info(void);   /* arch, compile flags */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTT_H */

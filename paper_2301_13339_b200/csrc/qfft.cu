@@ -1,0 +1,295 @@
+// qfft.cu — capped QTT-FFT / QTT-iFFT on sm_100a (PAPER.md P:309-321,
+// P:370-382; construction of SURVEY.md §8(c) O2, inverse O6, centering O3).
+//
+// One CTA per transform keeps every core in shared memory and runs the whole
+// serial chain on chip.  Stage p (p = d..1; a = axis(p), t = bit(p),
+// s = b_a - t + 1):
+//   p = d : core_d[:, al, :] <- core_d[:,0,:] + (-1)^al core_d[:,1,:]
+//   p < d : cut ranks p..d-1 double: core_p <- [core_p[:,0,:] | (-1)^al
+//           core_p[:,1,:]], core_q <- blockdiag(core_q, phi_q core_q),
+//           core_d <- vstack(core_d, phi_d core_d), phi_q(1) = exp(-i pi /
+//           2^{bit(q)-t}) for axis(q) = a; then ROUND_LOCAL(p).
+// ROUND_LOCAL(p) is evaluated without the LQ sweep of the oracle: the right
+// Gram matrices GR_c = R_c R_c^H of the doubled cores are built right-to-left
+// once per stage, and the truncation of cut c uses the Hermitian
+// K_c = M_c GR_c M_c^H, whose eigenvalues are the squared singular values of
+// the cut-c unfolding and whose eigenvectors are its left singular vectors
+// (the same truncated tensor as LQ + SVD, in exact arithmetic).
+// The doubled cores are never stored: they are formed on the fly from the
+// compact cores (ranks <= RS_XF) kept in shared memory.
+#include "qtt_kernels.h"
+
+namespace qtt {
+
+static constexpr int NT = 256;
+static constexpr int RS = RS_XF;
+static constexpr int CSZ = 2 * RS * RS;
+static constexpr int R2 = 2 * RS;
+
+struct XfSmem {
+  cplx C[MAXD][CSZ];
+  cplx D[R2 * 2 * R2];
+  cplx Eb[RS * 2 * R2];
+  cplx G[2][R2 * R2];
+  cplx T[2 * R2 * R2];
+  cplx Sm[RS * R2];
+  EigSmem<R2> E;
+  int r[MAXD + 1];
+  int rb[MAXD + 1];
+  int rk;
+  double tau2;
+};
+
+// twiddle of position q (1-based) in the stage of axis a, bit t, slice be
+__device__ __forceinline__ cplx phi_of(const XfParams& P, int q, int a, int t, int be) {
+  if (be == 0 || P.axis[q - 1] != a) return cmk(1.0, 0.0);
+  const int k = P.bit[q - 1] - t;   // >= 1
+  return cexpipi(-1.0 / (double)(1 << k));
+}
+
+// doubled core of position q (p < q <= d) of the current stage into S.D;
+// dims (2 a0) x 2 x (q < d ? 2 b0 : 1)
+__device__ void build_doubled(XfSmem& S, const XfParams& P, int q, int a, int t) {
+  const int d = P.d;
+  const int a0 = S.r[q - 1], b0 = S.r[q];
+  const cplx* c = S.C[q - 1];
+  const cplx ph = phi_of(P, q, a, t, 1);
+  if (q < d) {
+    const int rows = 2 * a0, cols = 2 * b0;
+    for (int e = threadIdx.x; e < rows * 2 * cols; e += NT) {
+      int i = e % rows, be = (e / rows) & 1, j = e / (2 * rows);
+      cplx v = czero();
+      if (i < a0 && j < b0) v = c[i + a0 * be + 2 * a0 * j];
+      else if (i >= a0 && j >= b0) {
+        v = c[(i - a0) + a0 * be + 2 * a0 * (j - b0)];
+        if (be) v = cmul(ph, v);
+      }
+      S.D[e] = v;
+    }
+  } else {
+    const int rows = 2 * a0;
+    for (int e = threadIdx.x; e < rows * 2; e += NT) {
+      int i = e % rows, be = e / rows;
+      cplx v = (i < a0) ? c[i + a0 * be] : c[(i - a0) + a0 * be];
+      if (i >= a0 && be) v = cmul(ph, v);
+      S.D[e] = v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams P) {
+  const XfProb& pr = probs[blockIdx.x];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  XfSmem& S = *reinterpret_cast<XfSmem*>(smraw);
+  constexpr int LD = EigSmem<R2>::LD;
+  const int tid = threadIdx.x;
+  const int d = P.d;
+  // load (conj for the inverse)
+  for (int q = tid; q <= d; q += NT) S.r[q] = pr.in_ranks[q];
+  __syncthreads();
+  for (int q = 0; q < d; ++q) {
+    const int n = S.r[q] * 2 * S.r[q + 1];
+    for (int e = tid; e < n; e += NT) {
+      cplx v = pr.in_cores[(size_t)q * SLOT + e];
+      S.C[q][e] = P.inverse ? cconj(v) : v;
+    }
+  }
+  __syncthreads();
+  for (int p = d; p >= 1; --p) {
+    const int a = P.axis[p - 1], t = P.bit[p - 1];
+    if (p == d) {
+      const int a0 = S.r[d - 1];
+      cplx* c = S.C[d - 1];
+      for (int i = tid; i < a0; i += NT) {
+        cplx x0 = c[i], x1 = c[i + a0];
+        c[i] = cadd(x0, x1);
+        c[i + a0] = csub(x0, x1);
+      }
+      __syncthreads();
+      continue;
+    }
+    // ---- right Gram chain GR_c, c = d-1 .. p, into global slots
+    build_doubled(S, P, d, a, t);
+    __syncthreads();
+    {
+      const int rows = 2 * S.r[d - 1];
+      for (int e = tid; e < rows * rows; e += NT) {
+        int i = e % rows, j = e / rows;
+        cplx s = czero();
+        for (int be = 0; be < 2; ++be) s = cfma_bc(S.D[i + rows * be], S.D[j + rows * be], s);
+        S.G[0][e] = s;
+        pr.gr[(size_t)(d - 1) * GR_XF + e] = s;
+      }
+    }
+    __syncthreads();
+    int gc = 0;
+    for (int c = d - 1; c >= p + 1; --c) {
+      build_doubled(S, P, c, a, t);
+      __syncthreads();
+      const int rows = 2 * S.r[c - 1], cols = 2 * S.r[c];
+      // T[be] = D[be] G   (rows x cols)
+      for (int e = tid; e < 2 * rows * cols; e += NT) {
+        int i = e % rows, be = (e / rows) & 1, j = e / (2 * rows);
+        cplx s = czero();
+        for (int l = 0; l < cols; ++l)
+          s = cfma(S.D[i + rows * be + 2 * rows * l], S.G[gc][l + cols * j], s);
+        S.T[i + rows * j + rows * cols * be] = s;
+      }
+      __syncthreads();
+      // Gn = sum_be T[be] D[be]^H
+      for (int e = tid; e < rows * rows; e += NT) {
+        int i = e % rows, j = e / rows;
+        cplx s = czero();
+        for (int be = 0; be < 2; ++be)
+          for (int l = 0; l < cols; ++l)
+            s = cfma_bc(S.T[i + rows * l + rows * cols * be], S.D[j + rows * be + 2 * rows * l], s);
+        S.G[gc ^ 1][e] = s;
+        pr.gr[(size_t)(c - 1) * GR_XF + e] = s;
+      }
+      __syncthreads();
+      gc ^= 1;
+    }
+    // ---- rank bounds of the LQ sweep (oracle ROUND_LOCAL (i)): rb_c
+    if (tid == 0) {
+      S.rb[d] = 1;
+      for (int c = d - 1; c >= p; --c) {
+        int v = 2 * S.r[c], w = 2 * S.rb[c + 1];
+        S.rb[c] = v < w ? v : w;
+      }
+    }
+    // ---- E = concat(core_p)
+    {
+      const int a0 = S.r[p - 1], b0 = S.r[p];
+      const cplx* c = S.C[p - 1];
+      for (int e = tid; e < a0 * 2 * 2 * b0; e += NT) {
+        int i = e % a0, al = (e / a0) & 1, j = e / (2 * a0);
+        cplx v = (j < b0) ? c[i + 2 * a0 * j] : c[i + a0 + 2 * a0 * (j - b0)];
+        if (j >= b0 && al) v = cmk(-v.x, -v.y);
+        S.Eb[e] = v;
+      }
+    }
+    __syncthreads();
+    // ---- truncation sweep, c = p .. d-1
+    int ap = S.r[p - 1];
+    for (int c = p; c <= d - 1; ++c) {
+      const int rows = 2 * ap, cols = 2 * S.r[c];
+      for (int e = tid; e < cols * cols; e += NT) S.G[0][e] = pr.gr[(size_t)c * GR_XF + e];
+      __syncthreads();
+      // T = M G  (rows x cols), M = Eb (ld rows)
+      for (int e = tid; e < rows * cols; e += NT) {
+        int i = e % rows, j = e / rows;
+        cplx s = czero();
+        for (int l = 0; l < cols; ++l) s = cfma(S.Eb[i + rows * l], S.G[0][l + cols * j], s);
+        S.T[e] = s;
+      }
+      __syncthreads();
+      // K = T M^H
+      for (int e = tid; e < rows * rows; e += NT) {
+        int i = e % rows, j = e / rows;
+        cplx s = czero();
+        for (int l = 0; l < cols; ++l) s = cfma_bc(S.T[i + rows * l], S.Eb[j + rows * l], s);
+        S.E.A[0][i + LD * j] = s;
+      }
+      __syncthreads();
+      if (c == p) {
+        double tr = 0.0;
+        if (tid < rows) tr = S.E.A[0][tid + LD * tid].x;
+        tr = block_sum<NT>(tr, S.E.red);
+        if (tid == 0) S.tau2 = P.eps * P.eps * tr / (double)(d - 1);
+        __syncthreads();
+      }
+      const cplx* U = jacobi_eig<R2, NT>(S.E, rows, P.status);
+      if (tid == 0) {
+        int mp = rows < S.rb[c] ? rows : S.rb[c];
+        S.rk = rank_rule(S.E.lam, mp, S.tau2, P.rmax, P.ctol);
+      }
+      __syncthreads();
+      const int rk = S.rk;
+      // new core c = U_r  (ap x 2 x rk)
+      for (int e = tid; e < rows * rk; e += NT) {
+        int i = e % rows, r = e / rows;
+        S.C[c - 1][i + rows * r] = U[i + LD * r];
+      }
+      // Sm = U_r^H M  (rk x cols)
+      for (int e = tid; e < rk * cols; e += NT) {
+        int r = e % rk, l = e / rk;
+        cplx s = czero();
+        for (int i = 0; i < rows; ++i) s = cfmac(U[i + LD * r], S.Eb[i + rows * l], s);
+        S.Sm[e] = s;
+      }
+      __syncthreads();
+      // next E = Sm * doubled(core c+1)
+      {
+        const int q = c + 1;
+        const int a1 = S.r[c];
+        const cplx* cn = S.C[q - 1];
+        if (q < d) {
+          const int b1 = S.r[q];
+          for (int e = tid; e < rk * 2 * 2 * b1; e += NT) {
+            int r = e % rk, be = (e / rk) & 1, j = e / (2 * rk);
+            cplx s = czero();
+            if (j < b1) {
+              for (int i = 0; i < a1; ++i) s = cfma(S.Sm[r + rk * i], cn[i + a1 * be + 2 * a1 * j], s);
+            } else {
+              for (int i = 0; i < a1; ++i)
+                s = cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be + 2 * a1 * (j - b1)], s);
+              if (be) s = cmul(phi_of(P, q, a, t, 1), s);
+            }
+            S.Eb[e] = s;
+          }
+        } else {
+          for (int e = tid; e < rk * 2; e += NT) {
+            int r = e % rk, be = e / rk;
+            cplx s0 = czero(), s1 = czero();
+            for (int i = 0; i < a1; ++i) {
+              s0 = cfma(S.Sm[r + rk * i], cn[i + a1 * be], s0);
+              s1 = cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be], s1);
+            }
+            if (be) s1 = cmul(phi_of(P, q, a, t, 1), s1);
+            S.Eb[e] = cadd(s0, s1);
+          }
+        }
+      }
+      __syncthreads();
+      if (tid == 0) S.r[c] = rk;
+      __syncthreads();
+      ap = rk;
+    }
+    for (int e = tid; e < ap * 2; e += NT) S.C[d - 1][e] = S.Eb[e];
+    __syncthreads();
+  }
+  // ---- reversal (core'_q = core_{d+1-q}, rank indices swapped), center,
+  //      conj (inverse), scale core 1
+  for (int q = tid; q <= d; q += NT) pr.out_ranks[q] = S.r[d - q];
+  for (int q = 1; q <= d; ++q) {
+    const cplx* c = S.C[d - q];
+    const int a0 = S.r[d - q], b0 = S.r[d - q + 1];   // source dims (a0, 2, b0)
+    cplx ph = cmk(1.0, 0.0);
+    if (P.do_center) {
+      const int ax = P.axis[d - q], tt = P.bit[d - q], b = P.bits[ax];
+      const int m = b + 1 - tt;
+      unsigned long long num = ((unsigned long long)P.shift[ax] << (m - 1)) & ((1ull << b) - 1ull);
+      if (num) ph = cexpipi((double)num / (double)(1ull << (b - 1)));
+    }
+    cplx* o = pr.out_cores + (size_t)(q - 1) * SLOT;
+    for (int e = tid; e < a0 * 2 * b0; e += NT) {
+      int i = e % b0, be = (e / b0) & 1, j = e / (2 * b0);   // out (b0, 2, a0): (i, be, j)
+      cplx v = c[j + a0 * be + 2 * a0 * i];
+      if (be) v = cmul(ph, v);
+      if (P.inverse) v = cconj(v);
+      if (q == 1) v = cscale(v, P.scale);
+      o[e] = v;
+    }
+  }
+}
+
+cudaError_t setup_xf_kernels() {
+  return cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(XfSmem));
+}
+
+cudaError_t launch_transform(const XfProb* probs_dev, int nprob, const XfParams& prm, cudaStream_t st) {
+  k_transform<<<nprob, NT, sizeof(XfSmem), st>>>(probs_dev, prm);
+  return cudaGetLastError();
+}
+
+}  // namespace qtt

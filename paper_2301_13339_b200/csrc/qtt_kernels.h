@@ -1,0 +1,107 @@
+// qtt_kernels.h — device-side problem descriptors and launchers used by the
+// C-ABI layer (api.cu).  Internal to libqtt; not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qtt_dev.cuh"
+
+namespace qtt {
+
+// A TT core slot holds up to RC x 2 x RC complex entries (RC = 16), stored
+// compact column-major: element (a, be, b) of an (r0, 2, r1) core at
+// a + r0*be + 2*r0*b (so the r0 x 2r1 and 2r0 x r1 unfoldings of P:234 are
+// plain column-major views of the same memory).
+static constexpr int RC = 16;
+static constexpr int SLOT = 2 * RC * RC;
+static constexpr int NBLK_MAX = 296;      // 2 x 148 SMs
+static constexpr int MAXD = 30;
+static constexpr int RS_XF = 10;          // compact rank capacity of the transform kernels
+static constexpr int RH_MAX = 8;          // Rhat cap supported by the Hadamard rounding
+
+// ---------------------------------------------------------------- TT-SVD
+struct DecProb {
+  const double* x;   // input array (caller layout)
+  int layout, bx, d;
+  double* Wa;        // ping-pong unfolding buffers
+  double* Wb;
+  double* part;      // per-CTA partial Grams [NBLK_MAX][32*32]
+  double* proj;      // current projector (<= 32 x 16, ld 32)
+  double* tau2;      // per-cut threshold tau^2
+  cplx* cores;       // d slots
+  int* ranks;        // r_0..r_d
+};
+struct DecParams {
+  double eps;
+  int rmax;
+  double ctol;
+  int* status;
+};
+cudaError_t setup_ttsvd_kernels();
+cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st);
+
+// ------------------------------------------------------------- transforms
+struct XfProb {
+  const cplx* in_cores;
+  const int* in_ranks;
+  cplx* out_cores;
+  int* out_ranks;
+  cplx* gr;          // right-Gram scratch: MAXD slots of (2 RS_XF)^2
+};
+struct XfParams {
+  int d;
+  int bits[2];
+  int axis[MAXD];
+  int bit[MAXD];
+  double eps;
+  int rmax;
+  double ctol;
+  int inverse;       // conj in / conj out
+  double scale;      // multiplies core 1 of the output
+  int do_center;
+  long long shift[2];
+  int* status;
+};
+static constexpr int GR_XF = 4 * RS_XF * RS_XF;   // complex per GR slot
+cudaError_t setup_xf_kernels();
+cudaError_t launch_transform(const XfProb* probs_dev, int nprob, const XfParams& prm, cudaStream_t st);
+
+// ------------------------------------------------- Hadamard + TT-rounding
+struct HrProb {
+  const cplx* f_cores;
+  const int* f_ranks;
+  const cplx* g_cores;
+  const int* g_ranks;
+  cplx* out_cores;
+  int* out_ranks;
+  cplx* gr;          // MAXD slots of 64 x 64
+};
+struct HrParams {
+  int d;
+  double eps;
+  int rmax;
+  double ctol;
+  int* status;
+};
+static constexpr int GR_HR = 64 * 64;
+cudaError_t setup_hr_kernels();
+cudaError_t launch_hadamard_round(const HrProb* probs_dev, int nprob, const HrParams& prm, cudaStream_t st);
+
+// -------------------------------------------------------------- expansion
+struct ExProb {
+  const cplx* cores;
+  const int* ranks;
+  double* y;         // output (caller layout)
+  double* lsplit;    // 256 x 32 scratch (column-major, ld 256)
+};
+struct ExParams {
+  int d;
+  int layout;
+  int bx;
+  int imag;          // 0: y = Re(full), 1: y = Im(full)
+};
+cudaError_t setup_expand_kernels();
+cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& prm, cudaStream_t st);
+
+}  // namespace qtt

@@ -1,0 +1,85 @@
+"""The C-ABI library (no GPU needed): it loads, exports every function
+include/qtt.h declares, and its host-side validation and workspace sizing
+behave as documented."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2301_13339_b200 import build as B
+from paper_2301_13339_b200 import qtt as Q
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    B.build()
+    return Q.lib()
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "qtt.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qtt_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(L):
+    names = _declared()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(L, n), n
+    assert sorted(Q.SYMBOLS) == names
+
+
+def test_build_info_names_sm100a(L):
+    assert "sm_100a" in Q.build_info()
+
+
+def test_status_strings(L):
+    assert L.qtt_status_string(0) == b"QTT_OK"
+    assert L.qtt_status_string(1) == b"QTT_EINVAL"
+    assert L.qtt_status_string(5) == b"QTT_ENOMEM"
+
+
+def test_workspace_bytes_validation(L):
+    dec, fft = Q.trunc(1e-3, 10), Q.trunc(1e-3, 8)
+    n18 = Q.qtt_workspace_bytes(Q.shape(2, [9, 9], "interleaved"), dec, fft)
+    n20 = Q.qtt_workspace_bytes(Q.shape(2, [10, 10], "interleaved"), dec, fft)
+    assert 0 < n18 < n20
+    # batch with a shared kernel grows the plan
+    nb = Q.qtt_workspace_bytes(Q.shape(2, [9, 9], "interleaved", batch=4), dec, fft)
+    assert nb > n18
+    bad = [
+        (Q.shape(3, [9, 9]), dec, fft),                          # D
+        (Q.shape(2, [9, 8], "interleaved"), dec, fft),            # non-square interleave
+        (Q.shape(1, [40, 0]), dec, fft),                          # d > 30
+        (Q.shape(1, [1, 0]), dec, fft),                           # d < 2
+        (Q.shape(2, [9, 9], "1d"), dec, fft),                     # layout mismatch
+        (Q.shape(2, [9, 9], "interleaved"), Q.trunc(-1.0, 10), fft),
+        (Q.shape(2, [9, 9], "interleaved"), Q.trunc(1e-3, 0), fft),
+        (Q.shape(2, [9, 9], "interleaved"), dec, Q.trunc(1e-3, 9)),   # Rhat > 8
+    ]
+    for s, a, b in bad:
+        assert L.qtt_workspace_bytes(ctypes.byref(s), ctypes.byref(a), ctypes.byref(b), 1) == 0
+
+
+def test_invalid_arguments_fail_before_any_device_work(L):
+    h = ctypes.c_void_p()
+    s = Q.shape(3, [9, 9])
+    st = L.qtt_decompose(None, ctypes.byref(s), ctypes.byref(Q.trunc(1e-3, 10)), None, 0, None,
+                         None, ctypes.byref(h))
+    assert st == Q.QTT_EINVAL
+    assert b"D must be" in L.qtt_last_error()
+    s = Q.shape(1, [12, 0])
+    st = L.qtt_conv_full(None, None, None, ctypes.byref(s), ctypes.byref(Q.trunc(1e-3, 10)),
+                         ctypes.byref(Q.trunc(1e-3, 8)), None, 1.0, None, 0, None, None, None)
+    assert st == Q.QTT_EINVAL
+    # workspace too small is reported as ENOMEM, not a device fault
+    st = L.qtt_conv_full(ctypes.c_void_p(256), ctypes.c_void_p(256), ctypes.c_void_p(256),
+                         ctypes.byref(s), ctypes.byref(Q.trunc(1e-3, 10)),
+                         ctypes.byref(Q.trunc(1e-3, 8)), None, 1.0, ctypes.c_void_p(256), 1024,
+                         None, None, None)
+    assert st == Q.QTT_ENOMEM
