@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""bench.py — end-to-end QTT convolution throughput on B200 (BASELINE.json metric:
+"end-to-end full-array elements/s (decompose+QTT conv+expand), fraction of HBM
+roofline").
+
+One step = one call of qtt_conv_full (Alg. 2: TT-SVD of
+f and g, QTT-FFTs, Hadamard + rounding, QTT-iFFT, expansion) over one input
+of the chosen config, inputs resident in HBM, L2 flushed between steps.
+N > 1 (torchrun): every rank runs its own independent problem (distinct
+signal seed, same kernel) — the path shards over independent problems with
+no data-path collective ("scaling": "weak"); the max over ranks of the device
+time is used.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+  python bench.py --impl reference ...   # the float64 CPU oracle, same metric
+
+Prints ONE JSON line on rank 0.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2301_13339_b200 import synth  # noqa: E402
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0          # GB/s, B200_PROFILING.md fallback
+# FP64 FMA peak from unit counts (B200_PROFILING.md / DESIGN.md §6):
+# 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--eps", type=float, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload(cfg, eps):
+    p = synth.problem(cfg)
+    e = p["eps"][0] if eps is None else eps
+    desc = (f"{cfg}: {'1D' if p['D'] == 1 else '2D'} 2^{p['b']}"
+            f"{'' if p['D'] == 1 else 'x2^' + str(p['b'])} float64 SAR-like "
+            f"(d={p['d']}, {p['layout']} bits, batch {p['batch']}), eps={e:g}, caps "
+            f"(R_max, Rhat_max)=({p['rmax']},{p['rhat']}), periodic conv shift n/2")
+    return p, e, desc
+
+
+def make_inputs(cfg, rank):
+    p = synth.problem(cfg)
+    if p["batch"] > 1:
+        f = np.stack([synth.signal(cfg, index=rank * p["batch"] + i) for i in range(p["batch"])])
+    else:
+        f = synth.signal(cfg, index=rank)
+    g = synth.kernel(p["D"], p["b"], synth.CONFIGS[cfg]["w"])
+    return f, g
+
+
+def peaks():
+    try:
+        m = json.load(open(MEASURED))
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6
+                          for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------- CPU oracle leg
+def oracle_run(cfg, eps, seconds, rank=0):
+    """The float64 oracle (test infrastructure, bench cpu_baseline leg) on a
+    bounded sample: whole pipelines of the same config until `seconds`."""
+    import oracle as O
+    p = synth.problem(cfg)
+    f, g = make_inputs(cfg, rank)
+    fs = f if p["batch"] > 1 else f[None]
+    dec = (eps, p["rmax"], p["cluster_tol"])
+    fft = (eps, p["rhat"], p["cluster_tol"])
+    n_el, t0, runs = 0, time.perf_counter(), 0
+    while True:
+        O.conv_pipeline(fs[runs % len(fs)], g, p["layout"], dec, fft, p["shift"], p["scale"])
+        runs += 1
+        n_el += 1 << p["d"]
+        el = time.perf_counter() - t0
+        if el >= seconds or runs >= 1000:
+            break
+    cores = len(os.sched_getaffinity(0))
+    return {"value": n_el / el, "unit": "elements/s", "cores": cores, "kind": "oracle",
+            "sample": f"{runs} whole pipeline(s) of {cfg} ({1 << p['d']} elements each) "
+                      f"in {el:.1f} s, numpy/LAPACK float64 on {cores} host threads"}
+
+
+# ------------------------------------------------------------- chain flops
+def chain_flops(d, rhat):
+    """Algorithmic FP64 flops of the small-core chain (SURVEY §8(d) 'small-core
+    work O(d^2 Rhat^3)'): per truncated cut an m x m Hermitian
+    eigenproblem (m = 2 Rhat, ~9 m^3 complex = 36 m^3 real flops) plus forming
+    K = M GR M^H (8 (m n^2 + m^2 n), n = 2 Rhat)."""
+    m = n = 2 * rhat
+    per_cut = 36 * m ** 3 + 8 * (m * n * n + m * m * n)
+    cuts = d * (d - 1) // 2
+    return {"qfft": 2 * cuts * per_cut, "qifft": cuts * per_cut,
+            "hadamard_round": (d - 1) * (36 * m ** 3 + 8 * (m * 64 * 64 + m * m * 64))}
+
+
+# ------------------------------------------------------------------- ours
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2301_13339_b200 import build as B
+    from paper_2301_13339_b200 import qtt as Q
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    B.build()
+    cfg = a.config
+    p, eps, desc = workload(cfg, a.eps)
+    f, g = make_inputs(cfg, rank)
+    batch = p["batch"]
+    d = p["d"]
+    n = 1 << d
+    D = p["D"]
+    bits = [p["b"], p["b"]] if D == 2 else [p["b"], 0]
+    shp = Q.shape(D, bits, p["layout"], batch, n, 0, n)
+    dec = Q.trunc(eps, p["rmax"], p["cluster_tol"])
+    fft = Q.trunc(eps, p["rhat"], p["cluster_tol"])
+    nb = Q.qtt_workspace_bytes(shp, dec, fft)
+    ws = torch.empty(nb + 256, dtype=torch.uint8, device=dev)
+    f_d = torch.from_numpy(np.ascontiguousarray(f).reshape(-1)).to(dev)
+    g_d = torch.from_numpy(np.ascontiguousarray(g).reshape(-1)).to(dev)
+    y_d = torch.empty(batch * n, dtype=torch.float64, device=dev)
+    f_h = torch.from_numpy(np.ascontiguousarray(f).reshape(-1)).pin_memory()
+    g_h = torch.from_numpy(np.ascontiguousarray(g).reshape(-1)).pin_memory()
+    y_h = torch.empty(batch * n, dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    def step():
+        Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, dec, fft, p["shift"],
+                        p["scale"], ws.data_ptr(), nb, sp)
+
+    def e2e_step():
+        f_d.copy_(f_h, non_blocking=True)
+        g_d.copy_(g_h, non_blocking=True)
+        step()
+        y_h.copy_(y_d, non_blocking=True)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, steps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        for e0, e1 in evs:
+            flush.zero_()
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return sum(e0.elapsed_time(e1) for e0, e1 in evs)
+
+    # correctness guard of this run: numeric status + ranks
+    rep = Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, dec, fft, p["shift"],
+                          p["scale"], ws.data_ptr(), nb, sp, report=True)
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    l0 = Q.qtt_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        ms = timed(step, a.steps)
+        barrier()
+    launches = Q.qtt_launch_count() - l0
+    # e2e through host buffers (pinned), copies inside the timed region
+    for _ in range(max(1, a.warmup // 2)):
+        e2e_step()
+    barrier()
+    ms_e2e = timed(e2e_step, a.steps)
+    barrier()
+    # stage profile (separate, untimed-by-the-metric pass)
+    Q.qtt_profile_enable(True)
+    stages = {}
+    npf = 3
+    for _ in range(npf):
+        flush.zero_()
+        step()
+        for k, v in Q.qtt_profile_read().items():
+            stages[k] = stages.get(k, 0.0) + v / npf
+    Q.qtt_profile_enable(False)
+
+    if world > 1:
+        t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ms_e2e = float(t[0]), float(t[1])
+    el_step = batch * n
+    total_el = world * el_step * a.steps
+    value = total_el / (ms / 1e3)
+    e2e = total_el / (ms_e2e / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+    hbm, src = peaks()
+    ng = 1
+    nf = batch
+    # algorithmic bytes per stage: TT-SVD two-read floor 16 B/el per
+    # input; expansion 8 B/el written
+    alg = {"ttsvd": ("hbm", 16.0 * n * (nf + ng)), "expand": ("hbm", 8.0 * n * nf)}
+    cf = chain_flops(d, p["rhat"])
+    for k in cf:
+        alg[k] = ("alu", float(cf[k]) * (nf if k != "qfft" else (nf + ng) / 2))
+    dom = max(stages, key=stages.get) if stages else "ttsvd"
+    bound, amount = alg[dom]
+    dur = stages.get(dom, 0.0) / 1e3
+    if bound == "hbm":
+        ach = amount / dur / 1e9 if dur else None
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm if ach else None, "traffic": None,
+                "kernel": dom, "peak_source": src}
+    else:
+        ach = amount / dur / 1e12 if dur else None
+        roof = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": ach / FP64_PEAK_TFLOPS if ach else None, "traffic": None,
+                "kernel": dom, "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
+    passes = {}
+    for k in ("ttsvd", "expand"):
+        if k in stages and stages[k] > 0:
+            gbs = alg[k][1] / (stages[k] / 1e3) / 1e9
+            passes[k] = {"ms": round(stages[k], 4), "alg_GBps": round(gbs, 1),
+                         "frac_hbm": round(gbs / hbm, 4)}
+    line = {
+        "metric": "end-to-end full-array elements/s (decompose+QTT conv+expand), fraction of HBM roofline",
+        "value": value, "unit": "elements/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded SAR-like scatterers + sinc kernel, BASELINE.json configs)",
+        "config": {"workload": desc, "global_batch": world * batch, "elements_per_step": el_step,
+                   "parallelism": f"independent problems x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "hbm_fraction_e2e_floor": (40.0 * el_step * world / (ms / 1e3 / a.steps) / 1e9) / hbm,
+        "e2e": {"value": e2e, "unit": "elements/s",
+                "h2d_bytes_per_step": int(f_h.numel() * 8 + g_h.numel() * 8),
+                "d2h_bytes_per_step": int(y_h.numel() * 8)},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "stages_ms": {k: round(v, 4) for k, v in stages.items()},
+        "hbm_passes": passes,
+        "clocks": clk.summary(),
+        "ranks": {"f": rep["ranks_f"], "g": rep["ranks_g"], "out": rep["ranks_out"]},
+    }
+    if not a.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = oracle_run(cfg, eps, a.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# -------------------------------------------------------------- reference
+def run_reference(a):
+    """--impl reference: the float64 oracle as it stands, timed on the host
+    cores, same metric/config/unit; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    p, eps, desc = workload(a.config, a.eps)
+    per_step = max(1.0, 60.0 / max(1, a.steps + a.warmup))
+    for _ in range(a.warmup):
+        oracle_run(a.config, eps, 0.0)
+    vals = [oracle_run(a.config, eps, per_step) for _ in range(a.steps)]
+    v = sum(x["value"] for x in vals) / len(vals)
+    el_step = (1 << p["d"]) * p["batch"]
+    cb = dict(vals[-1])
+    cb["value"] = v
+    line = {
+        "metric": "end-to-end full-array elements/s (decompose+QTT conv+expand), fraction of HBM roofline",
+        "value": v, "unit": "elements/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": el_step / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": desc, "global_batch": p["batch"], "elements_per_step": el_step},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

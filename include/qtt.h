@@ -147,9 +147,10 @@ void qtt_destroy(qtt_tt_t t);
 /* TEST-ONLY: Hermitian eigendecomposition of the n x n (n <= 32) complex
  * matrix A (device, column-major interleaved re/im doubles) by the CTA Jacobi
  * solver every truncation of the path uses.  lam (device, n): eigenvalues in
- * descending order; U (device, n x n complex): eigenvectors; sweeps (device
- * int): Jacobi sweeps used.  Stream-ordered, no sync. */
-int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, void* stream);
+ * descending order; U (device, n x n complex): eigenvectors; sweeps (device,
+ * 6 ints): fp64 sweeps, fp32 sweeps, cycles of the 4 phases of the last
+ * repetition; reps: repeat count (timing).  Stream-ordered. */
+int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, void* stream);
 
 /* TEST-ONLY: build a handle from host cores (shape->batch tensors; tensor i,
  * core k occupies the slot of 512 complex starting at ((i*d)+k)*512, compact
@@ -158,6 +159,16 @@ int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, void
 qtt_status qtt_debug_tt_from_host(const qtt_shape* shape, const void* cores_host,
                                   const int* ranks_host, int rcap, void* ws,
                                   size_t ws_bytes, void* stream, qtt_tt_t* out);
+
+/* Stage profiling of qtt_conv_full: when enabled, CUDA events are recorded
+ * on the call's stream at the stage boundaries.  qtt_profile_read syncs on
+ * the last call's final event and writes n >= 5 stage times (ms): [0] TT-SVD
+ * of f and g, [1] forward QTT-FFTs, [2] Hadamard + rounding, [3] QTT-iFFT,
+ * [4] expansion; returns the number written (0 if nothing was recorded). */
+void qtt_profile_enable(int on);
+int qtt_profile_read(float* ms_host, int n);
+/* Total number of kernels this library has launched in the process. */
+long long qtt_launch_count(void);
 
 const char* qtt_status_string(qtt_status s);
 const char* qtt_last_error(void);   /* thread-local, never NULL */

@@ -7,6 +7,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -16,6 +17,11 @@
 #include "qtt_kernels.h"
 
 using namespace qtt;
+
+namespace qtt {
+static std::atomic<long long> g_launches{0};
+void count_launches(int n) { g_launches += n; }
+}  // namespace qtt
 
 #define QTT_XSTR(x) #x
 #define QTT_STR(x) QTT_XSTR(x)
@@ -48,6 +54,20 @@ qtt_status fail(qtt_status s, const char* fmt, ...) {
 qtt_status cuda_check(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return QTT_OK;
   return fail(QTT_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+// ---- optional stage profiling (CUDA events on the caller's stream)
+enum { PROF_STAGES = 5, PROF_MARKS = PROF_STAGES + 1 };
+int g_prof = 0;
+cudaEvent_t g_ev[PROF_MARKS] = {};
+int g_ev_ok = 0;
+void prof_mark(int i, cudaStream_t st) {
+  if (!g_prof) return;
+  if (!g_ev_ok) {
+    for (int k = 0; k < PROF_MARKS; ++k) cudaEventCreate(&g_ev[k]);
+    g_ev_ok = 1;
+  }
+  cudaEventRecord(g_ev[i], st);
 }
 
 std::once_flag g_setup_once;
@@ -142,7 +162,7 @@ struct DecScratch {
 };
 DecScratch take_dec(Carver& cv, int d) {
   DecScratch s{};
-  if (d > 13) {
+  if (d > 12) {
     s.Wa = cv.take<double>((size_t)RC << (d - 5));
     s.Wb = cv.take<double>((size_t)RC << (d - 6));
     s.part = cv.take<double>((size_t)NBLK_MAX * 1024);
@@ -264,6 +284,7 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
   qtt_status r;
   if ((r = run_transform(fpart, s, fft, 0, nullptr, 1.0, cv, status, st))) return r;
   if ((r = run_transform(gpart, s, fft, 0, shift, 1.0, cv, status, st))) return r;
+  if (cv.base) prof_mark(2, st);
   std::vector<HrProb> hr(nf);
   for (int i = 0; i < nf; ++i) {
     HrProb& p = hr[i];
@@ -292,8 +313,11 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
                         "copy descriptors")))
       return r;
     if ((r = cuda_check(launch_hadamard_round(hp, nf, H, st), "hadamard/round launch"))) return r;
+    prof_mark(3, st);
   }
-  return run_transform(iv, s, fft, 1, nullptr, scale, cv, status, st);
+  r = run_transform(iv, s, fft, 1, nullptr, scale, cv, status, st);
+  if (cv.base) prof_mark(4, st);
+  return r;
 }
 
 qtt_status check_ws(const Carver& cv, void* ws, size_t ws_bytes) {
@@ -486,6 +510,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   int* status = cv.take<int>(64);
   TTAlloc F = take_tt(cv, nf, d), G = take_tt(cv, ng, d), Y = take_tt(cv, nf, d);
   if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
+  prof_mark(0, st);
   // Step 1-2: all signals and the kernel(s) in one batched TT-SVD
   {
     const int d_ = d;
@@ -510,11 +535,13 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
     DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status};
     if ((r = cuda_check(launch_ttsvd(dp, nf + ng, d_, prm, st), "TT-SVD launch"))) return r;
   }
+  prof_mark(1, st);
   // Step 3
   if ((r = run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, shift, scale, Y, cv, status, st)))
     return r;
   // Step 4
   if ((r = run_expand(Y.cores, Y.ranks, nf, d, y, ys, shape, 0, cv, st))) return r;
+  prof_mark(5, st);
   if (cv.off > ws_bytes) return fail(QTT_ENOMEM, "internal: workspace plan overflow");
   if (rep_host) {
     cudaEventRecord(e1, st);
@@ -558,6 +585,21 @@ qtt_status qtt_ranks(qtt_tt_t t, int index, int* ranks_host, int cap) {
 }
 
 int qtt_ndims(qtt_tt_t t) { return t ? t->d : 0; }
+
+void qtt_profile_enable(int on) { g_prof = on ? 1 : 0; }
+
+int qtt_profile_read(float* ms_host, int n) {
+  if (!g_ev_ok || !ms_host || n < PROF_STAGES) return 0;
+  if (cudaEventSynchronize(g_ev[PROF_MARKS - 1]) != cudaSuccess) return 0;
+  for (int k = 0; k < PROF_STAGES; ++k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_ev[k], g_ev[k + 1]);
+    ms_host[k] = ms;
+  }
+  return PROF_STAGES;
+}
+
+long long qtt_launch_count(void) { return qtt::g_launches.load(); }
 
 qtt_status qtt_debug_tt_from_host(const qtt_shape* shape, const void* cores_host, const int* ranks_host, int rcap,
                                   void* ws, size_t ws_bytes, void* stream, qtt_tt_t* out) {

@@ -7,23 +7,40 @@
 namespace qtt {
 static constexpr int NT = 256;
 
-__global__ void __launch_bounds__(NT) k_debug_eigh(const cplx* A, int n, double* lam, cplx* U, int* sweeps) {
+template <int NMAX>
+__global__ void __launch_bounds__(NT) k_debug_eigh(const cplx* A, int n, double* lam, cplx* U, int* sweeps,
+                                                   int reps) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  EigSmem<32>& E = *reinterpret_cast<EigSmem<32>*>(smraw);
-  constexpr int LD = EigSmem<32>::LD;
-  for (int e = threadIdx.x; e < n * n; e += NT) E.A[0][(e % n) + LD * (e / n)] = A[e];
-  __syncthreads();
-  const cplx* V = jacobi_eig<32, NT>(E, n, nullptr);
+  EigSmem<NMAX>& E = *reinterpret_cast<EigSmem<NMAX>*>(smraw);
+  constexpr int LD = EigSmem<NMAX>::LD;
+  const cplx* V = nullptr;
+  for (int r = 0; r < reps; ++r) {
+    for (int e = threadIdx.x; e < n * n; e += NT) E.A[0][(e % n) + LD * (e / n)] = A[e];
+    __syncthreads();
+    V = jacobi_eig<NMAX, NT>(E, n, nullptr);
+  }
   for (int e = threadIdx.x; e < n * n; e += NT) U[e] = V[(e % n) + LD * (e / n)];
   for (int i = threadIdx.x; i < n; i += NT) lam[i] = E.lam[i];
-  if (threadIdx.x == 0) *sweeps = E.sweeps;
+  if (threadIdx.x == 0) {
+    sweeps[0] = E.sweeps;
+    sweeps[1] = E.sweeps32;
+    for (int k = 0; k < 4; ++k) sweeps[2 + k] = (int)E.tphase[k];
+  }
 }
 }  // namespace qtt
 
-extern "C" int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, void* stream) {
+extern "C" int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, void* stream) {
   using namespace qtt;
-  if (n < 1 || n > 32) return QTT_EINVAL;
-  cudaFuncSetAttribute(k_debug_eigh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem<32>));
-  k_debug_eigh<<<1, NT, sizeof(EigSmem<32>), (cudaStream_t)stream>>>((const cplx*)A, n, lam, (cplx*)U, sweeps);
+  if (n < 1 || n > 32 || reps < 1) return QTT_EINVAL;
+  if (n <= 16) {
+    cudaFuncSetAttribute(k_debug_eigh<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem<16>));
+    k_debug_eigh<16><<<1, NT, sizeof(EigSmem<16>), (cudaStream_t)stream>>>((const cplx*)A, n, lam, (cplx*)U,
+                                                                           sweeps, reps);
+  } else {
+    cudaFuncSetAttribute(k_debug_eigh<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem<32>));
+    k_debug_eigh<32><<<1, NT, sizeof(EigSmem<32>), (cudaStream_t)stream>>>((const cplx*)A, n, lam, (cplx*)U,
+                                                                           sweeps, reps);
+  }
+  count_launches(1);
   return cudaGetLastError() == cudaSuccess ? QTT_OK : QTT_ECUDA;
 }

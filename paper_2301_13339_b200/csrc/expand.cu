@@ -241,6 +241,7 @@ cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& pr
   if (d <= 13) {
     int nb = (int)(((1ull << d) + 255) / 256);
     k_expand_small<<<dim3(nb, nprob), 256, 0, st>>>(probs_dev, prm);
+    count_launches(1);
     return cudaGetLastError();
   }
   k_expand_prep<<<nprob, 256, PREP_SMEM, st>>>(probs_dev, prm);
@@ -249,6 +250,7 @@ cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& pr
   int per = (int)((nchunks + target - 1) / target);
   int nb = (int)((nchunks + per - 1) / per);
   k_expand_main<<<dim3(nb, nprob), NT, sizeof(ExSmem), st>>>(probs_dev, prm, per);
+  count_launches(2);
   return cudaGetLastError();
 }
 

@@ -235,6 +235,7 @@ cudaError_t setup_hr_kernels() {
 
 cudaError_t launch_hadamard_round(const HrProb* probs_dev, int nprob, const HrParams& prm, cudaStream_t st) {
   k_hadamard_round<<<nprob, NT, sizeof(HrSmem), st>>>(probs_dev, prm);
+  count_launches(1);
   return cudaGetLastError();
 }
 

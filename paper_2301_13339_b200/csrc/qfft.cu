@@ -23,6 +23,18 @@ namespace qtt {
 
 static constexpr int NT = 256;
 static constexpr int RS = RS_XF;
+
+// optional phase timing (compile with -DQTT_XF_TIMING): cycles per phase of
+// CTA 0 are accumulated into XfProb::gr scratch tail (debug builds only)
+#ifdef QTT_XF_TIMING
+#define XT_DECL long long xt_t0 = clock64(), xt_acc[6] = {0, 0, 0, 0, 0, 0};
+#define XT_MARK(k) { long long _t = clock64(); xt_acc[k] += _t - xt_t0; xt_t0 = _t; }
+#define XT_DUMP(ptr) if (threadIdx.x == 0) { for (int _k = 0; _k < 6; ++_k) ((long long*)(ptr))[_k] = xt_acc[_k]; }
+#else
+#define XT_DECL
+#define XT_MARK(k)
+#define XT_DUMP(ptr)
+#endif
 static constexpr int CSZ = 2 * RS * RS;
 static constexpr int R2 = 2 * RS;
 
@@ -95,6 +107,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
     }
   }
   __syncthreads();
+  XT_DECL
   for (int p = d; p >= 1; --p) {
     const int a = P.axis[p - 1], t = P.bit[p - 1];
     if (p == d) {
@@ -149,6 +162,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       __syncthreads();
       gc ^= 1;
     }
+    XT_MARK(0)
     // ---- rank bounds of the LQ sweep (oracle ROUND_LOCAL (i)): rb_c
     if (tid == 0) {
       S.rb[d] = 1;
@@ -173,6 +187,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
     int ap = S.r[p - 1];
     for (int c = p; c <= d - 1; ++c) {
       const int rows = 2 * ap, cols = 2 * S.r[c];
+      XT_MARK(5)
       for (int e = tid; e < cols * cols; e += NT) S.G[0][e] = pr.gr[(size_t)c * GR_XF + e];
       __syncthreads();
       // T = M G  (rows x cols), M = Eb (ld rows)
@@ -198,7 +213,9 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
         if (tid == 0) S.tau2 = P.eps * P.eps * tr / (double)(d - 1);
         __syncthreads();
       }
+      XT_MARK(1)
       const cplx* U = jacobi_eig<R2, NT>(S.E, rows, P.status);
+      XT_MARK(2)
       if (tid == 0) {
         int mp = rows < S.rb[c] ? rows : S.rb[c];
         S.rk = rank_rule(S.E.lam, mp, S.tau2, P.rmax, P.ctol);
@@ -254,10 +271,13 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       if (tid == 0) S.r[c] = rk;
       __syncthreads();
       ap = rk;
+      XT_MARK(3)
     }
     for (int e = tid; e < ap * 2; e += NT) S.C[d - 1][e] = S.Eb[e];
     __syncthreads();
   }
+  XT_MARK(4)
+  XT_DUMP(pr.gr + (size_t)MAXD * GR_XF - 8)
   // ---- reversal (core'_q = core_{d+1-q}, rank indices swapped), center,
   //      conj (inverse), scale core 1
   for (int q = tid; q <= d; q += NT) pr.out_ranks[q] = S.r[d - q];
@@ -289,6 +309,7 @@ cudaError_t setup_xf_kernels() {
 
 cudaError_t launch_transform(const XfProb* probs_dev, int nprob, const XfParams& prm, cudaStream_t st) {
   k_transform<<<nprob, NT, sizeof(XfSmem), st>>>(probs_dev, prm);
+  count_launches(1);
   return cudaGetLastError();
 }
 

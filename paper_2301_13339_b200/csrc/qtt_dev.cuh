@@ -94,25 +94,46 @@ __device__ __forceinline__ void raise_status(int* status, int bit) {
 
 // -------------------------------------------------------- Jacobi eigensolver
 // Hermitian A (n x n, n <= NMAX) in shared memory, column-major with leading
-// dimension NMAX+1.  Cyclic two-sided Jacobi with the round-robin parallel
-// ordering (n/2 disjoint rotations per round, one fused J^H A J update per
-// round).  On return lam[0..n-1] holds the eigenvalues in descending order
-// and U (column-major, ld NMAX+1) the matching orthonormal eigenvectors.
-// Stops after a sweep in which no pair needed a rotation (see below).
+// dimension NMAX+1.  Mixed-precision cyclic two-sided Jacobi, round-robin
+// parallel ordering (n/2 disjoint rotations per round, one fused J^H A J and
+// V J update per round with a fixed thread -> element map):
+//   1. fp32 sweeps on a float copy of A (cheap rotations) -> basis V;
+//   2. V re-orthonormalised in fp64 by two Newton-Schulz steps, A' = V^H A V;
+//   3. fp64 polish sweeps on A' (V accumulated), pair (p,q) rotated iff
+//      |a_pq| > max(2 eps ||A||_F, eps sqrt|a_pp a_qq|), eps = 2^-53; stops
+//      after a sweep without rotations.
+// The result is that of a plain fp64 Jacobi (same stopping rule); stage 1
+// only supplies a starting basis.  On return lam[0..n-1] holds the
+// eigenvalues in descending order and the returned pointer (column-major, ld
+// NMAX+1, inside the scratch) the matching orthonormal eigenvectors.
+struct JacPar {
+  double cs;      // J[i][i]
+  double cox;     // J[partner][i] (complex)
+  double coy;
+  double nd;      // exact new diagonal when rotated
+  int partner;
+  int rot;
+};
+struct JacParF {
+  float cs, cox, coy, nd;
+  int partner, rot;
+};
+
 template <int NMAX>
 struct EigSmem {
   static constexpr int LD = NMAX + 1;
   cplx A[2][NMAX * LD];
   cplx V[2][NMAX * LD];
-  double cs[NMAX + 1];
-  cplx co[NMAX + 1];
-  int partner[NMAX + 1];
-  double nd[NMAX + 1];
-  int rot[NMAX + 1];
+  float2 Af[2][NMAX * LD];
+  float2 Vf[2][NMAX * LD];
+  JacPar par[NMAX + 1];
+  JacParF parf[NMAX + 1];
   double lam[NMAX];
+  int rank_of[NMAX];
   double red[32];
-  int cur;
   int sweeps;
+  int sweeps32;
+  long long tphase[4];   // clock64 cycles: fp32 sweeps, basis change, fp64 sweeps, sort
 };
 
 template <int NT>
@@ -134,29 +155,218 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// A is read from E.A[0] (caller fills the full Hermitian matrix).  Result:
-// E.lam (descending) and a pointer to the sorted eigenvectors (column-major,
-// ld NMAX+1) inside E, valid until the next call.  Non-convergence raises
-// ST_NOCONV in *status.
+// ---- fast reciprocal / rsqrt: one MUFU op (fp32 approx) or MUFU + Newton
+// steps to full fp64 precision (no IEEE slow-path subroutine calls)
+__device__ __forceinline__ float frsqrt_fast(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float frcp_fast(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double drcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double drsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+// round-robin pair of slot k in round r (N even): circle method
+__device__ __forceinline__ void rr_pair(int N, int r, int k, int& p, int& q) {
+  if (k == 0) { p = N - 1; q = r; return; }
+  p = r + k;
+  if (p >= N - 1) p -= N - 1;
+  q = r - k;
+  if (q < 0) q += N - 1;
+}
+
+// ---- float complex helpers
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // a*b + c
+  return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, c.y)));
+}
+__device__ __forceinline__ float2 ffmac2(float2 a, float2 b, float2 c) {  // conj(a)*b + c
+  return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(-a.y, b.x, c.y)));
+}
+__device__ __forceinline__ float2 fscale2(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+
+// new value of element (i,j) of J^H A J given the rotation parameters
+__device__ __forceinline__ cplx jac_elem(const cplx* A, int LD, int i, int j, const JacPar& Pi,
+                                         const JacPar& Pj) {
+  if (Pi.rot && i == j) return cmk(Pi.nd, 0.0);
+  if (Pi.rot && Pj.partner == i) return czero();
+  const int ip = Pi.partner, jp = Pj.partner;
+  const cplx oi = cmk(Pi.cox, Pi.coy), oj = cmk(Pj.cox, Pj.coy);
+  cplx t0 = cfma(oj, A[i + LD * jp], cscale(A[i + LD * j], Pj.cs));
+  cplx t1 = cfma(oj, A[ip + LD * jp], cscale(A[ip + LD * j], Pj.cs));
+  return cfmac(oi, t1, cscale(t0, Pi.cs));
+}
+__device__ __forceinline__ float2 jac_elem_f(const float2* A, int LD, int i, int j, const JacParF& Pi,
+                                             const JacParF& Pj) {
+  if (Pi.rot && i == j) return make_float2(Pi.nd, 0.f);
+  if (Pi.rot && Pj.partner == i) return make_float2(0.f, 0.f);
+  const int ip = Pi.partner, jp = Pj.partner;
+  const float2 oi = make_float2(Pi.cox, Pi.coy), oj = make_float2(Pj.cox, Pj.coy);
+  float2 t0 = ffma2(oj, A[i + LD * jp], fscale2(A[i + LD * j], Pj.cs));
+  float2 t1 = ffma2(oj, A[ip + LD * jp], fscale2(A[ip + LD * j], Pj.cs));
+  return ffmac2(oi, t1, fscale2(t0, Pi.cs));
+}
+
+// fixed thread -> element map over the padded NP x NP index square
+template <int NMAX, int NT, class F>
+__device__ __forceinline__ void for_elems(int n, F&& f) {
+  constexpr int NP = NMAX <= 16 ? 16 : 32;
+  constexpr int EPT = NP * NP / NT;
+  if (NP == 16 || n <= 16) {
+    const int i = threadIdx.x & 15, j = threadIdx.x >> 4;
+    if (threadIdx.x < 256 && i < n && j < n) f(i, j);
+  } else {
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+      const int e = threadIdx.x + NT * k;
+      const int i = e & (NP - 1), j = e / NP;
+      if (i < n && j < n) f(i, j);
+    }
+  }
+}
+
+// C = op(X) * Y for n x n complex matrices in smem (ld LD); CONJX: X^H
+template <int NMAX, int NT, bool CONJX>
+__device__ __forceinline__ void small_mm(cplx* C, const cplx* X, const cplx* Y, int n, int LD) {
+  for_elems<NMAX, NT>(n, [&](int i, int j) {
+    cplx s = czero();
+    for (int l = 0; l < n; ++l) s = CONJX ? cfmac(X[l + LD * i], Y[l + LD * j], s) : cfma(X[i + LD * l], Y[l + LD * j], s);
+    C[i + LD * j] = s;
+  });
+}
+
 template <int NMAX, int NT>
 __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x;
   const int N = n + (n & 1);
-  for (int e = tid; e < n * n; e += NT) {
-    int i = e % n, j = e / n;
-    E.V[0][i + LD * j] = cmk(i == j ? 1.0 : 0.0, 0.0);
-  }
+  const int half = N / 2;
   double nrm2 = 0.0;
   for (int e = tid; e < n * n; e += NT) {
     int i = e % n, j = e / n;
-    nrm2 += cabs2(E.A[0][i + LD * j]);
+    const cplx v = E.A[0][i + LD * j];
+    nrm2 += cabs2(v);
+    E.Af[0][i + LD * j] = make_float2((float)v.x, (float)v.y);
+    E.Vf[0][i + LD * j] = make_float2(i == j ? 1.f : 0.f, 0.f);
   }
-  nrm2 = block_sum<NT>(nrm2, E.red);
-  // rotate (p,q) iff |a_pq| > max(1e-18 ||A||_F, 2^-53 sqrt|a_pp a_qq|):
-  // high relative accuracy down to the formation noise of A; converged when a
-  // whole sweep rotates nothing.
-  const double floor_abs = 1e-18 * sqrt(nrm2);
+  nrm2 = block_sum<NT>(nrm2, E.red);     // contains barriers
+  long long tc0 = clock64();
+  // ---------------- stage 1: fp32 sweeps
+  {
+    const float EPSF = 5.9604645e-8f;
+    const float floor2f = (float)(4.0 * 3.5527136788005e-15 * nrm2);   // (2 eps_f)^2 ||A||^2
+    int cur = 0;
+    int sw = 0;
+    bool conv = (n <= 1);
+    for (; sw < 16 && !conv; ++sw) {
+      int any_sweep = 0;
+      for (int round = 0; round < N - 1; ++round) {
+        const float2* A = E.Af[cur];
+        int did = 0;
+        if (tid < half) {
+          int p, q;
+          rr_pair(N, round, tid, p, q);
+          if (p >= n || q >= n) {
+            if (p < n) { JacParF z{1.f, 0.f, 0.f, 0.f, p, 0}; E.parf[p] = z; }
+            if (q < n) { JacParF z{1.f, 0.f, 0.f, 0.f, q, 0}; E.parf[q] = z; }
+          } else {
+            const float a = A[p + LD * p].x, c = A[q + LD * q].x;
+            const float2 b = A[p + LD * q];
+            const float ab2 = b.x * b.x + b.y * b.y;
+            const float thr2 = fmaxf(floor2f, EPSF * EPSF * fabsf(a * c));
+            if (!(ab2 > thr2)) {
+              JacParF zp{1.f, 0.f, 0.f, 0.f, q, 0}, zq{1.f, 0.f, 0.f, 0.f, p, 0};
+              E.parf[p] = zp;
+              E.parf[q] = zq;
+            } else {
+              const float inv_ab = frsqrt_fast(ab2);
+              const float ab = ab2 * inv_ab;
+              const float zeta = (c - a) * 0.5f * inv_ab;
+              const float az = fminf(fabsf(zeta), 1e18f);
+              const float y = fmaf(az, az, 1.f);
+              float t = frcp_fast(az + y * frsqrt_fast(y));
+              if (zeta < 0.f) t = -t;
+              const float cc = frsqrt_fast(fmaf(t, t, 1.f));
+              const float sf = t * cc * inv_ab;
+              JacParF pp{cc, -sf * b.x, sf * b.y, a - t * ab, q, 1};
+              JacParF pq{cc, sf * b.x, sf * b.y, c + t * ab, p, 1};
+              E.parf[p] = pp;
+              E.parf[q] = pq;
+              did = 1;
+            }
+          }
+        }
+        if (!__syncthreads_or(did)) continue;
+        any_sweep = 1;
+        float2* An = E.Af[cur ^ 1];
+        const float2* V = E.Vf[cur];
+        float2* Vn = E.Vf[cur ^ 1];
+        for_elems<NMAX, NT>(n, [&](int i, int j) {
+          const JacParF Pi = E.parf[i], Pj = E.parf[j];
+          An[i + LD * j] = jac_elem_f(A, LD, i, j, Pi, Pj);
+          Vn[i + LD * j] = ffma2(make_float2(Pj.cox, Pj.coy), V[i + LD * Pj.partner], fscale2(V[i + LD * j], Pj.cs));
+        });
+        __syncthreads();
+        cur ^= 1;
+      }
+      conv = !any_sweep;
+    }
+    if (tid == 0) E.sweeps32 = sw;
+    if (tid == 0) { long long t = clock64(); E.tphase[0] = t - tc0; tc0 = t; }
+    // V (fp64) <- Vf; two Newton-Schulz steps V <- V (3 I - V^H V) / 2
+    for (int e = tid; e < n * n; e += NT) {
+      int i = e % n, j = e / n;
+      const float2 v = E.Vf[cur][i + LD * j];
+      E.V[0][i + LD * j] = cmk((double)v.x, (double)v.y);
+    }
+    __syncthreads();
+    for (int it = 0; it < 2; ++it) {
+      small_mm<NMAX, NT, true>(E.V[1], E.V[0], E.V[0], n, LD);    // G = V^H V
+      __syncthreads();
+      for_elems<NMAX, NT>(n, [&](int i, int j) {                 // H = (3I - G)/2 (in place)
+        cplx g = E.V[1][i + LD * j];
+        E.V[1][i + LD * j] = cmk((i == j ? 1.5 : 0.0) - 0.5 * g.x, -0.5 * g.y);
+      });
+      __syncthreads();
+      small_mm<NMAX, NT, false>(E.A[1], E.V[0], E.V[1], n, LD);   // V H
+      __syncthreads();
+      for_elems<NMAX, NT>(n, [&](int i, int j) { E.V[0][i + LD * j] = E.A[1][i + LD * j]; });
+      __syncthreads();
+    }
+    // A' = V^H A V  (A in E.A[0], V in E.V[0])
+    small_mm<NMAX, NT, false>(E.A[1], E.A[0], E.V[0], n, LD);       // A V
+    __syncthreads();
+    small_mm<NMAX, NT, true>(E.V[1], E.V[0], E.A[1], n, LD);        // V^H (A V)
+    __syncthreads();
+    for_elems<NMAX, NT>(n, [&](int i, int j) {                      // symmetrise
+      const cplx a = E.V[1][i + LD * j], b = E.V[1][j + LD * i];
+      E.A[0][i + LD * j] = cmk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+    });
+    __syncthreads();
+  }
+  if (tid == 0) { long long t = clock64(); E.tphase[1] = t - tc0; tc0 = t; }
+  // ---------------- stage 2: fp64 polish sweeps
+  const double EPSM = 1.1102230246251565e-16;
+  const double floor2 = 4.0 * EPSM * EPSM * nrm2;
   int cur = 0;
   bool conv = (n <= 1);
   int sweep = 0;
@@ -165,33 +375,52 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
     for (int round = 0; round < N - 1; ++round) {
       const cplx* A = E.A[cur];
       int did = 0;
-      if (tid < N / 2) {
+      if (tid < half) {
         int p, q;
-        if (tid == 0) { p = N - 1; q = round; }
-        else { p = (round + tid) % (N - 1); q = (round - tid + (N - 1)) % (N - 1); }
+        rr_pair(N, round, tid, p, q);
         if (p >= n || q >= n) {
-          if (p < n) { E.cs[p] = 1.0; E.co[p] = czero(); E.partner[p] = p; E.rot[p] = 0; }
-          if (q < n) { E.cs[q] = 1.0; E.co[q] = czero(); E.partner[q] = q; E.rot[q] = 0; }
+          if (p < n) { JacPar z{1.0, 0.0, 0.0, 0.0, p, 0}; E.par[p] = z; }
+          if (q < n) { JacPar z{1.0, 0.0, 0.0, 0.0, q, 0}; E.par[q] = z; }
         } else {
-          double a = A[p + LD * p].x, c = A[q + LD * q].x;
-          cplx b = A[p + LD * q];
-          double ab = sqrt(cabs2(b));
-          double thr = fmax(floor_abs, 1.1102230246251565e-16 * sqrt(fabs(a * c)));
-          if (!(ab > thr)) {
-            E.cs[p] = 1.0; E.co[p] = czero(); E.partner[p] = q; E.rot[p] = 0;
-            E.cs[q] = 1.0; E.co[q] = czero(); E.partner[q] = p; E.rot[q] = 0;
+          const double a = A[p + LD * p].x, c = A[q + LD * q].x;
+          const cplx b = A[p + LD * q];
+          const double ab2 = cabs2(b);
+          const double thr2 = fmax(floor2, EPSM * EPSM * fabs(a * c));
+          if (!(ab2 > thr2)) {
+            JacPar zp{1.0, 0.0, 0.0, 0.0, q, 0}, zq{1.0, 0.0, 0.0, 0.0, p, 0};
+            E.par[p] = zp;
+            E.par[q] = zq;
           } else {
-            double zeta = (c - a) / (2.0 * ab);
-            double t = 1.0 / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            if (zeta < 0.0) t = -t;
-            double cc = 1.0 / sqrt(1.0 + t * t);
-            double ss = t * cc;
-            cplx S = cmk(ss * b.x / ab, ss * b.y / ab);
-            E.cs[p] = cc; E.co[p] = cmk(-S.x, S.y);  // -conj(S)
-            E.cs[q] = cc; E.co[q] = S;
-            E.partner[p] = q; E.partner[q] = p;
-            E.nd[p] = a - t * ab; E.nd[q] = c + t * ab;
-            E.rot[p] = 1; E.rot[q] = 1;
+            const double dca = c - a;
+            double t, cc, sfb;   // sfb = t cc / |b|
+            double tab;          // t |b|
+            if (dca * dca > 4e8 * ab2) {
+              // small angle (|zeta| > 1e4): with u = 1/(c-a), q = |b|^2 u^2:
+              // t = |b| u (1 - q) + O(q^2 t), cos = 1 - t^2/2 + 3 t^4/8
+              const double u = drcp_nr(dca);
+              const double qq = ab2 * u * u;
+              const double t2 = qq * (1.0 - qq) * (1.0 - qq);
+              cc = fma(t2, fma(0.375, t2, -0.5), 1.0);
+              sfb = u * (1.0 - qq) * cc;                 // t cc / |b|
+              tab = ab2 * u * (1.0 - qq);               // t |b|
+              t = 0.0;
+            } else {
+              const double inv_ab = drsqrt_nr(ab2);
+              const double ab = ab2 * inv_ab;
+              const double zeta = dca * 0.5 * inv_ab;
+              const double az = fabs(zeta);
+              const double y = fma(az, az, 1.0);
+              t = drcp_nr(az + y * drsqrt_nr(y));
+              if (zeta < 0.0) t = -t;
+              cc = drsqrt_nr(fma(t, t, 1.0));
+              sfb = t * cc * inv_ab;
+              tab = t * ab;
+            }
+            (void)t;
+            JacPar pp{cc, -sfb * b.x, sfb * b.y, a - tab, q, 1};    // co_p = -conj(S)
+            JacPar pq{cc, sfb * b.x, sfb * b.y, c + tab, p, 1};     // co_q = S
+            E.par[p] = pp;
+            E.par[q] = pq;
             did = 1;
           }
         }
@@ -201,33 +430,17 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
       cplx* An = E.A[cur ^ 1];
       const cplx* V = E.V[cur];
       cplx* Vn = E.V[cur ^ 1];
-      for (int e = tid; e < 2 * n * n; e += NT) {
-        if (e < n * n) {
-          int i = e % n, j = e / n;
-          int ip = E.partner[i], jp = E.partner[j];
-          cplx val;
-          if (E.rot[i] && i == j) val = cmk(E.nd[i], 0.0);
-          else if (E.rot[i] && jp == i) val = czero();
-          else {
-            double ci = E.cs[i], cj = E.cs[j];
-            cplx oi = E.co[i], oj = E.co[j];
-            cplx t0 = cfma(oj, A[i + LD * jp], cscale(A[i + LD * j], cj));
-            cplx t1 = cfma(oj, A[ip + LD * jp], cscale(A[ip + LD * j], cj));
-            val = cfmac(oi, t1, cscale(t0, ci));
-          }
-          An[i + LD * j] = val;
-        } else {
-          int f = e - n * n;
-          int i = f % n, j = f / n;
-          int jp = E.partner[j];
-          Vn[i + LD * j] = cfma(E.co[j], V[i + LD * jp], cscale(V[i + LD * j], E.cs[j]));
-        }
-      }
+      for_elems<NMAX, NT>(n, [&](int i, int j) {
+        const JacPar Pi = E.par[i], Pj = E.par[j];
+        An[i + LD * j] = jac_elem(A, LD, i, j, Pi, Pj);
+        Vn[i + LD * j] = cfma(cmk(Pj.cox, Pj.coy), V[i + LD * Pj.partner], cscale(V[i + LD * j], Pj.cs));
+      });
       __syncthreads();
       cur ^= 1;
     }
     conv = !any_sweep;
   }
+  if (tid == 0) { long long t = clock64(); E.tphase[2] = t - tc0; tc0 = t; }
   // stable descending sort; eigenvectors to the free V buffer
   for (int i = tid; i < n; i += NT) {
     double li = E.A[cur][i + LD * i].x;
@@ -236,17 +449,18 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
       double lj = E.A[cur][j + LD * j].x;
       rk += (lj > li) || (lj == li && j < i);
     }
-    E.partner[i] = rk;
+    E.rank_of[i] = rk;
   }
   __syncthreads();
   cplx* U = E.V[cur ^ 1];
-  for (int i = tid; i < n; i += NT) E.lam[E.partner[i]] = E.A[cur][i + LD * i].x;
+  for (int i = tid; i < n; i += NT) E.lam[E.rank_of[i]] = E.A[cur][i + LD * i].x;
   for (int e = tid; e < n * n; e += NT) {
     int i = e % n, j = e / n;
-    U[i + LD * E.partner[j]] = E.V[cur][i + LD * j];
+    U[i + LD * E.rank_of[j]] = E.V[cur][i + LD * j];
   }
   if (tid == 0) E.sweeps = sweep;
   __syncthreads();
+  if (tid == 0) E.tphase[3] = clock64() - tc0;
   if (!conv && tid == 0) raise_status(status, ST_NOCONV);
   return U;
 }

@@ -9,6 +9,9 @@
 
 namespace qtt {
 
+// number of kernels launched by this library (bench evidence: gpu_launches)
+void count_launches(int n);
+
 // A TT core slot holds up to RC x 2 x RC complex entries (RC = 16), stored
 // compact column-major: element (a, be, b) of an (r0, 2, r1) core at
 // a + r0*be + 2*r0*b (so the r0 x 2r1 and 2r0 x r1 unfoldings of P:234 are

@@ -13,7 +13,7 @@
 //                     DMMA Gram of the next unfolding reshape(W_m, [2 r_m, .]).
 //   K2'/K3'           the same per step k > m on the shrinking W buffers.
 //   K4 k_finish       one CTA per tensor finishes the last steps in shared
-//                     memory (and does small tensors, d <= 13, entirely).
+//                     memory (and does small tensors, d <= 12, entirely).
 // Truncation: tau^2 = eps^2 ||x||^2 / (d-1) (reading Q1), rank =
 // RANK(lambda, tau^2, R_max, delta_c) on the Gram eigenvalues lambda = sigma^2.
 #include "qtt_dev.cuh"
@@ -73,31 +73,44 @@ __device__ __forceinline__ void gram_step(double (&acc)[10][2], const double (&a
 }
 
 // Reduce per-warp Gram fragments (acc) over the CTA into a full 32x32
-// matrix `out` (row-major == column-major, symmetric).  scratch >= 8*1024.
+// matrix `out` (row-major == column-major, symmetric) in a fixed order.
+// scratch holds >= NSCR*1024 doubles; the 8 warps go in 8/NSCR passes.
+template <int NSCR = 8>
 __device__ void gram_reduce_cta(const double (&acc)[10][2], double* scratch, double* out) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  double* mine = scratch + w * 1024;
-  int pi = 0;
+  double part[1024 / NT];
 #pragma unroll
-  for (int bi = 0; bi < 4; ++bi) {
+  for (int k = 0; k < 1024 / NT; ++k) part[k] = 0.0;
 #pragma unroll
-    for (int bj = bi; bj < 4; ++bj) {
+  for (int pass = 0; pass < 8 / NSCR; ++pass) {
+    if (w / NSCR == pass) {
+      double* mine = scratch + (w % NSCR) * 1024;
+      int pi = 0;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        int r = 8 * bi + (lane >> 2), c = 8 * bj + 2 * (lane & 3) + e;
-        mine[r * 32 + c] = acc[pi][e];
-        if (bi != bj) mine[c * 32 + r] = acc[pi][e];
+      for (int bi = 0; bi < 4; ++bi) {
+#pragma unroll
+        for (int bj = bi; bj < 4; ++bj) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            int r = 8 * bi + (lane >> 2), c = 8 * bj + 2 * (lane & 3) + e;
+            mine[r * 32 + c] = acc[pi][e];
+            if (bi != bj) mine[c * 32 + r] = acc[pi][e];
+          }
+          ++pi;
+        }
       }
-      ++pi;
     }
-  }
-  __syncthreads();
-  for (int e = tid; e < 1024; e += NT) {
-    double s = 0.0;
+    __syncthreads();
 #pragma unroll
-    for (int ww = 0; ww < NT / 32; ++ww) s += scratch[ww * 1024 + e];
-    out[e] = s;
+    for (int k = 0; k < 1024 / NT; ++k) {
+      const int e = tid + NT * k;
+#pragma unroll
+      for (int ww = 0; ww < NSCR; ++ww) part[k] += scratch[ww * 1024 + e];
+    }
+    __syncthreads();
   }
+#pragma unroll
+  for (int k = 0; k < 1024 / NT; ++k) out[tid + NT * k] = part[k];
   __syncthreads();
 }
 
@@ -396,7 +409,9 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
 }
 
 // ------------------------------------------------------------------- K4
-static constexpr int FIN_CAP = 8192;
+static constexpr int FIN_CAP = 4096;             // doubles of W_{k-1} the finisher holds
+static constexpr int FIN_COLS = FIN_CAP / RC;     // 256 columns at the rank cap
+static constexpr int FIN_D = 12;                  // d <= 12: whole TT-SVD in one CTA
 struct FinishSmem {
   double B[2][FIN_CAP];
   EigSmem<32> E;
@@ -424,7 +439,7 @@ __device__ void gram_smem(const double* M, int rows, int n, double* scratch, dou
     gram_step(acc, a, nb);
   }
   __syncthreads();
-  gram_reduce_cta(acc, scratch, G);
+  gram_reduce_cta<4>(acc, scratch, G);
 }
 
 __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart, int src_is_a,
@@ -506,7 +521,7 @@ size_t smem_step_solve() { return sizeof(StepSolveSmem); }
 size_t smem_finish() { return sizeof(FinishSmem); }
 
 int dec_nblk(int d) {
-  if (d <= 13) return 0;
+  if (d <= FIN_D) return 0;
   uint64_t nchunks = 1ull << (d - 12);
   return (int)(nchunks < (uint64_t)NBLK_MAX ? nchunks : (uint64_t)NBLK_MAX);
 }
@@ -536,33 +551,38 @@ cudaError_t setup_ttsvd_kernels() {
 
 // Launch the whole TT-SVD for nprob problems of equal d (device array probs).
 cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st) {
-  if (d <= 13) {
+  if (d <= FIN_D) {
     k_finish<<<dim3(1, nprob), NT, smem_finish(), st>>>(probs_dev, 1, 1, prm);
+    count_launches(1);
     return cudaGetLastError();
   }
   const int nblk = dec_nblk(d);
   k_level_gram<<<dim3(nblk, nprob), NT, smem_level_gram(), st>>>(probs_dev, nblk, prm.status);
   k_level_solve<<<dim3(1, nprob), NT, smem_level_solve(), st>>>(probs_dev, nblk, prm);
+  count_launches(2);
   // K3: W_m from x, Gram for step m+1
   int k = LVL_M;
   {
     uint64_t nch = (1ull << (d - k)) / 128;
     int nb = (int)(nch < (uint64_t)NBLK_MAX ? nch : (uint64_t)NBLK_MAX);
     k_project<true><<<dim3(nb, nprob), NT, smem_project(), st>>>(probs_dev, k, nb, 1);
+    count_launches(1);
     int src_is_a = 1;  // W_m lives in Wa
     int prev_nb = nb;
     ++k;
-    // steps while W_{k-1} has more than 512 columns
-    while ((1 << (d - k + 1)) > 512) {
+    // steps while W_{k-1} has more than FIN_COLS columns
+    while ((1 << (d - k + 1)) > FIN_COLS) {
       k_step_solve<<<dim3(1, nprob), NT, smem_step_solve(), st>>>(probs_dev, k, prev_nb, prm);
       uint64_t nc = (1ull << (d - k)) / 128;
       int nb2 = (int)(nc < (uint64_t)NBLK_MAX ? nc : (uint64_t)NBLK_MAX);
       k_project<false><<<dim3(nb2, nprob), NT, smem_project(), st>>>(probs_dev, k, nb2, src_is_a);
+      count_launches(2);
       src_is_a ^= 1;
       prev_nb = nb2;
       ++k;
     }
     k_finish<<<dim3(1, nprob), NT, smem_finish(), st>>>(probs_dev, k, src_is_a, prm);
+    count_launches(1);
   }
   return cudaGetLastError();
 }

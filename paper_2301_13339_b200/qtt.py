@@ -20,7 +20,8 @@ SYMBOLS = [
     "qtt_workspace_bytes", "qtt_decompose", "qtt_transform", "qtt_convolve",
     "qtt_to_full", "qtt_conv_full", "qtt_wait", "qtt_ranks", "qtt_ndims",
     "qtt_destroy", "qtt_status_string", "qtt_last_error", "qtt_build_info",
-    "qtt_debug_eigh", "qtt_debug_tt_from_host",
+    "qtt_debug_eigh", "qtt_debug_tt_from_host", "qtt_profile_enable", "qtt_profile_read",
+    "qtt_launch_count",
 ]
 
 
@@ -88,7 +89,13 @@ def lib():
     L.qtt_build_info.restype = ctypes.c_char_p
     L.qtt_build_info.argtypes = []
     L.qtt_debug_eigh.restype = I
-    L.qtt_debug_eigh.argtypes = [P, I, P, P, P, P]
+    L.qtt_debug_eigh.argtypes = [P, I, P, P, P, I, P]
+    L.qtt_profile_enable.restype = None
+    L.qtt_profile_enable.argtypes = [I]
+    L.qtt_profile_read.restype = I
+    L.qtt_profile_read.argtypes = [ctypes.POINTER(ctypes.c_float), I]
+    L.qtt_launch_count.restype = ctypes.c_longlong
+    L.qtt_launch_count.argtypes = []
     L.qtt_debug_tt_from_host.restype = I
     L.qtt_debug_tt_from_host.argtypes = [pS, P, ctypes.POINTER(ctypes.c_int), I, P, S, P, pH]
     _LIB = L
@@ -188,9 +195,9 @@ def build_info():
     return lib().qtt_build_info().decode()
 
 
-def qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, stream=0):
+def qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, stream=0, reps=1):
     """Test-only: the path's CTA Jacobi eigensolver on one Hermitian matrix."""
-    _check(lib().qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, stream))
+    _check(lib().qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, reps, stream))
 
 
 def qtt_debug_tt_from_host(shp, cores_c128, ranks_i32, rcap, ws_ptr, ws_bytes, stream=0, ws_owner=None):
@@ -200,3 +207,20 @@ def qtt_debug_tt_from_host(shp, cores_c128, ranks_i32, rcap, ws_ptr, ws_bytes, s
                                         ranks_i32.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
                                         rcap, ws_ptr, ws_bytes, stream, ctypes.byref(h)))
     return TT(h, ws_owner)
+
+
+STAGES = ["ttsvd", "qfft", "hadamard_round", "qifft", "expand"]
+
+
+def qtt_profile_enable(on=True):
+    lib().qtt_profile_enable(1 if on else 0)
+
+
+def qtt_profile_read():
+    buf = (ctypes.c_float * 8)()
+    n = lib().qtt_profile_read(buf, 8)
+    return {STAGES[i]: float(buf[i]) for i in range(n)}
+
+
+def qtt_launch_count():
+    return int(lib().qtt_launch_count())

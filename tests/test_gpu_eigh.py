@@ -19,12 +19,12 @@ def _gpu_eigh(A):
     a = torch.from_numpy(np.ascontiguousarray(A.T).view(np.float64).copy()).cuda()  # column-major
     lam = torch.empty(n, dtype=torch.float64, device="cuda")
     U = torch.empty(2 * n * n, dtype=torch.float64, device="cuda")
-    sw = torch.zeros(1, dtype=torch.int32, device="cuda")
+    sw = torch.zeros(8, dtype=torch.int32, device="cuda")
     Q.qtt_debug_eigh(a.data_ptr(), n, lam.data_ptr(), U.data_ptr(), sw.data_ptr(),
                      torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     u = U.cpu().numpy().view(np.complex128).reshape(n, n).T
-    return lam.cpu().numpy(), u, int(sw.item())
+    return lam.cpu().numpy(), u, int(sw[0].item())
 
 
 @pytest.mark.parametrize("n,decades,cplx", [(16, 2, True), (20, 10, True), (32, 12, False),
