@@ -230,7 +230,6 @@ qtt_status run_transform(const std::vector<XfProb>& hv, const qtt_shape* s, cons
   P.ctol = fft->cluster_tol;
   P.inverse = inverse;
   P.scale = inverse ? scale * ldexp(1.0, -P.d) : 1.0;
-  P.do_center = (!inverse && shift) ? 1 : 0;
   P.shift[0] = shift ? shift[0] : 0;
   P.shift[1] = (shift && s->D == 2) ? shift[1] : 0;
   P.status = status;
@@ -278,12 +277,11 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.out_cores = (isf ? Fh.cores : Gh.cores) + (size_t)j * d * SLOT;
     p.out_ranks = (isf ? Fh.ranks : Gh.ranks) + (size_t)j * 64;
     p.gr = cv.take<cplx>((size_t)MAXD * GR_XF);
+    p.do_center = (!isf && shift) ? 1 : 0;   // center the kernel's spectrum only (O3)
   }
-  // forward transforms: F's without centering, G's with it -> two launches
-  std::vector<XfProb> fpart(fw.begin(), fw.begin() + nf), gpart(fw.begin() + nf, fw.end());
+  // forward transforms of all F's and G's: one launch, one CTA each
   qtt_status r;
-  if ((r = run_transform(fpart, s, fft, 0, nullptr, 1.0, cv, status, st))) return r;
-  if ((r = run_transform(gpart, s, fft, 0, shift, 1.0, cv, status, st))) return r;
+  if ((r = run_transform(fw, s, fft, 0, shift, 1.0, cv, status, st))) return r;
   if (cv.base) prof_mark(2, st);
   std::vector<HrProb> hr(nf);
   for (int i = 0; i < nf; ++i) {
@@ -306,6 +304,7 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.out_cores = Y.cores + (size_t)i * d * SLOT;
     p.out_ranks = Y.ranks + (size_t)i * 64;
     p.gr = fw[i].gr;   // reuse the forward scratch
+    p.do_center = 0;
   }
   if (cv.base) {
     HrParams H{d, fft->eps, fft->rmax, fft->cluster_tol, status};
@@ -416,6 +415,7 @@ qtt_status qtt_transform(qtt_tt_t in, const qtt_trunc* fft, int inverse, const l
       v[i].out_cores = o.cores + (size_t)i * d * SLOT;
       v[i].out_ranks = o.ranks + (size_t)i * 64;
       v[i].gr = cv.take<cplx>((size_t)MAXD * GR_XF);
+      v[i].do_center = (!inverse && shift) ? 1 : 0;
     }
   };
   Carver dry(nullptr);

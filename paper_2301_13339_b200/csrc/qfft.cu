@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
     const cplx* c = S.C[d - q];
     const int a0 = S.r[d - q], b0 = S.r[d - q + 1];   // source dims (a0, 2, b0)
     cplx ph = cmk(1.0, 0.0);
-    if (P.do_center) {
+    if (pr.do_center) {
       const int ax = P.axis[d - q], tt = P.bit[d - q], b = P.bits[ax];
       const int m = b + 1 - tt;
       unsigned long long num = ((unsigned long long)P.shift[ax] << (m - 1)) & ((1ull << b) - 1ull);

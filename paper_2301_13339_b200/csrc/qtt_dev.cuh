@@ -329,6 +329,16 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
         cur ^= 1;
       }
       conv = !any_sweep;
+      if (!conv) {
+        // the fp64 polish converges quadratically from here: stop at 1e-4 ||A||_F
+        double off = 0.0;
+        for (int e = tid; e < n * n; e += NT) {
+          const int i = e % n, j = e / n;
+          if (i != j) { const float2 v = E.Af[cur][i + LD * j]; off += (double)v.x * v.x + (double)v.y * v.y; }
+        }
+        off = block_sum<NT>(off, E.red);
+        conv = off <= 1e-8 * nrm2;
+      }
     }
     if (tid == 0) E.sweeps32 = sw;
     if (tid == 0) { long long t = clock64(); E.tphase[0] = t - tc0; tc0 = t; }
@@ -439,6 +449,16 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
       cur ^= 1;
     }
     conv = !any_sweep;
+    if (!conv) {
+      // every |a_pq| <= 2 eps ||A||_F  =>  the next sweep would rotate nothing
+      double off = 0.0;
+      for (int e = tid; e < n * n; e += NT) {
+        const int i = e % n, j = e / n;
+        if (i != j) off += cabs2(E.A[cur][i + LD * j]);
+      }
+      off = block_sum<NT>(off, E.red);
+      conv = off <= floor2;
+    }
   }
   if (tid == 0) { long long t = clock64(); E.tphase[2] = t - tc0; tc0 = t; }
   // stable descending sort; eigenvectors to the free V buffer

@@ -51,6 +51,7 @@ struct XfProb {
   cplx* out_cores;
   int* out_ranks;
   cplx* gr;          // right-Gram scratch: MAXD slots of (2 RS_XF)^2
+  int do_center;     // multiply the forward output by the centering phase (O3)
 };
 struct XfParams {
   int d;
@@ -62,7 +63,6 @@ struct XfParams {
   double ctol;
   int inverse;       // conj in / conj out
   double scale;      // multiplies core 1 of the output
-  int do_center;
   long long shift[2];
   int* status;
 };
