@@ -90,6 +90,9 @@ typedef struct {
   int ranks_f[64], ranks_g[64], ranks_fh[64], ranks_gh[64], ranks_z[64],
       ranks_out[64];
   float ms_total;
+  int status_bits;   /* device status word: 1 non-finite input, 2 eigensolver
+                        failure (both errors), 16 = a tridiagonal eigensolve
+                        fell back to Jacobi (information) */
 } qtt_report;
 
 /* Bytes of workspace needed by qtt_conv_full (and enough for any single
@@ -145,12 +148,14 @@ int qtt_ndims(qtt_tt_t t);
 void qtt_destroy(qtt_tt_t t);
 
 /* TEST-ONLY: Hermitian eigendecomposition of the n x n (n <= 32) complex
- * matrix A (device, column-major interleaved re/im doubles) by the CTA Jacobi
- * solver every truncation of the path uses.  lam (device, n): eigenvalues in
+ * matrix A (device, column-major interleaved re/im doubles) by the small
+ * eigensolver every truncation of the path uses (mode 0: tridiagonal solver
+ * with Jacobi fallback; mode 1: Jacobi only).  lam (device, n): eigenvalues in
  * descending order; U (device, n x n complex): eigenvectors; sweeps (device,
- * 6 ints): fp64 sweeps, fp32 sweeps, cycles of the 4 phases of the last
- * repetition; reps: repeat count (timing).  Stream-ordered. */
-int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, void* stream);
+ * >= 2 ints): Jacobi sweeps, fallbacks taken; reps: repeat count (timing).
+ * Stream-ordered. */
+int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, int mode,
+                   void* stream);
 
 /* TEST-ONLY: build a handle from host cores (shape->batch tensors; tensor i,
  * core k occupies the slot of 512 complex starting at ((i*d)+k)*512, compact

@@ -556,8 +556,9 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
     cudaMemcpy(rep_host->ranks_out, Y.ranks, (d + 1) * sizeof(int), cudaMemcpyDeviceToHost);
     int hs = 0;
     cudaMemcpy(&hs, status, sizeof(int), cudaMemcpyDeviceToHost);
+    rep_host->status_bits = hs;
     if ((r = cuda_check(cudaGetLastError(), "report"))) return r;
-    if (hs) return fail(QTT_ENUMERIC, "numeric status 0x%x (1 = non-finite input, 2 = eigensolver)", hs);
+    if (hs & ST_ERRORS) return fail(QTT_ENUMERIC, "numeric status 0x%x (1 = non-finite input, 2 = eigensolver)", hs);
   }
   return QTT_OK;
 }
@@ -568,7 +569,7 @@ qtt_status qtt_wait(qtt_tt_t t) {
   if ((r = cuda_check(cudaStreamSynchronize(t->stream), "stream sync"))) return r;
   int hs = 0;
   if ((r = cuda_check(cudaMemcpy(&hs, t->status, sizeof(int), cudaMemcpyDeviceToHost), "status read"))) return r;
-  if (hs) return fail(QTT_ENUMERIC, "numeric status 0x%x (1 = non-finite input, 2 = eigensolver)", hs);
+  if (hs & ST_ERRORS) return fail(QTT_ENUMERIC, "numeric status 0x%x (1 = non-finite input, 2 = eigensolver)", hs);
   return QTT_OK;
 }
 

@@ -1,6 +1,7 @@
-// debug.cu — test-only entry point exposing the CTA Jacobi eigensolver used
-// by every truncated SVD of the path (qtt_dev.cuh), so tests can check it
-// against numpy.linalg.eigh on graded Hermitian spectra.
+// debug.cu — test-only entry point exposing the small Hermitian eigensolver
+// used by every truncated SVD of the path (qtt_dev.cuh: tridiagonal solver
+// with Jacobi fallback, or Jacobi alone), so tests can check it against
+// numpy.linalg.eigh.
 #include "../../include/qtt.h"
 #include "qtt_kernels.h"
 
@@ -9,37 +10,39 @@ static constexpr int NT = 256;
 
 template <int NMAX>
 __global__ void __launch_bounds__(NT) k_debug_eigh(const cplx* A, int n, double* lam, cplx* U, int* sweeps,
-                                                   int reps) {
+                                                   int reps, int mode) {
   extern __shared__ __align__(16) unsigned char smraw[];
   EigSmem<NMAX>& E = *reinterpret_cast<EigSmem<NMAX>*>(smraw);
   constexpr int LD = EigSmem<NMAX>::LD;
   const cplx* V = nullptr;
+  if (threadIdx.x == 0) { E.fallbacks = 0; E.sweeps = 0; }
   for (int r = 0; r < reps; ++r) {
     for (int e = threadIdx.x; e < n * n; e += NT) E.A[0][(e % n) + LD * (e / n)] = A[e];
     __syncthreads();
-    V = jacobi_eig<NMAX, NT>(E, n, nullptr);
+    V = mode ? jacobi_eig<NMAX, NT>(E, n, nullptr) : eig_small<NMAX, NT>(E, n, n, nullptr);
   }
   for (int e = threadIdx.x; e < n * n; e += NT) U[e] = V[(e % n) + LD * (e / n)];
   for (int i = threadIdx.x; i < n; i += NT) lam[i] = E.lam[i];
   if (threadIdx.x == 0) {
     sweeps[0] = E.sweeps;
-    sweeps[1] = E.sweeps32;
-    for (int k = 0; k < 4; ++k) sweeps[2 + k] = (int)E.tphase[k];
+    sweeps[1] = E.fallbacks;
+    for (int k = 0; k < 5; ++k) sweeps[2 + k] = (int)E.u.tr.tph[k];
   }
 }
 }  // namespace qtt
 
-extern "C" int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, void* stream) {
+extern "C" int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, int mode,
+                              void* stream) {
   using namespace qtt;
   if (n < 1 || n > 32 || reps < 1) return QTT_EINVAL;
   if (n <= 16) {
     cudaFuncSetAttribute(k_debug_eigh<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem<16>));
     k_debug_eigh<16><<<1, NT, sizeof(EigSmem<16>), (cudaStream_t)stream>>>((const cplx*)A, n, lam, (cplx*)U,
-                                                                           sweeps, reps);
+                                                                           sweeps, reps, mode);
   } else {
     cudaFuncSetAttribute(k_debug_eigh<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem<32>));
     k_debug_eigh<32><<<1, NT, sizeof(EigSmem<32>), (cudaStream_t)stream>>>((const cplx*)A, n, lam, (cplx*)U,
-                                                                           sweeps, reps);
+                                                                           sweeps, reps, mode);
   }
   count_launches(1);
   return cudaGetLastError() == cudaSuccess ? QTT_OK : QTT_ECUDA;

@@ -175,13 +175,14 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
       if (tid == 0) S.tau2 = P.eps * P.eps * tr / (double)(d - 1);
       __syncthreads();
     }
-    const cplx* U = jacobi_eig<2 * RH, NT>(S.E, rows, P.status);
+    eig_values<2 * RH, NT>(S.E, rows);
     if (tid == 0) {
       int mp = rows < S.rb[c] ? rows : S.rb[c];
       S.rk = rank_rule(S.E.lam, mp, S.tau2, P.rmax, P.ctol);
     }
     __syncthreads();
     const int rk = S.rk;
+    const cplx* U = eig_vectors<2 * RH, NT>(S.E, rows, rk, P.status);
     cplx* oc = pr.out_cores + (size_t)(c - 1) * SLOT;
     for (int e = tid; e < rows * rk; e += NT) {
       int i = e % rows, r = e / rows;

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
         __syncthreads();
       }
       XT_MARK(1)
-      const cplx* U = jacobi_eig<R2, NT>(S.E, rows, P.status);
+      eig_values<R2, NT>(S.E, rows);
       XT_MARK(2)
       if (tid == 0) {
         int mp = rows < S.rb[c] ? rows : S.rb[c];
@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       }
       __syncthreads();
       const int rk = S.rk;
+      const cplx* U = eig_vectors<R2, NT>(S.E, rows, rk, P.status);
       // new core c = U_r  (ap x 2 x rk)
       for (int e = tid; e < rows * rk; e += NT) {
         int i = e % rows, r = e / rows;

@@ -87,7 +87,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // ------------------------------------------------------------ status word
-enum { ST_OK = 0, ST_NONFINITE = 1, ST_NOCONV = 2, ST_RANKCAP = 4 };
+enum { ST_OK = 0, ST_NONFINITE = 1, ST_NOCONV = 2, ST_RANKCAP = 4, ST_FALLBACK = 16 };
+enum { ST_ERRORS = ST_NONFINITE | ST_NOCONV };
 __device__ __forceinline__ void raise_status(int* status, int bit) {
   if (status) atomicOr(status, bit);
 }
@@ -119,23 +120,6 @@ struct JacParF {
   int partner, rot;
 };
 
-template <int NMAX>
-struct EigSmem {
-  static constexpr int LD = NMAX + 1;
-  cplx A[2][NMAX * LD];
-  cplx V[2][NMAX * LD];
-  float2 Af[2][NMAX * LD];
-  float2 Vf[2][NMAX * LD];
-  JacPar par[NMAX + 1];
-  JacParF parf[NMAX + 1];
-  double lam[NMAX];
-  int rank_of[NMAX];
-  double red[32];
-  int sweeps;
-  int sweeps32;
-  long long tphase[4];   // clock64 cycles: fp32 sweeps, basis change, fp64 sweeps, sort
-};
-
 template <int NT>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -154,6 +138,384 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   __syncthreads();
   return s;
 }
+
+// ---------------------------------------------- tridiagonal eigensolver
+// Latency-oriented Hermitian eigensolver used first for every small Gram
+// matrix (the Jacobi solver below is the fallback).  Split in two calls so
+// eigenvectors are computed only for the ranks the truncation keeps:
+//   trid_values:  A/||A||_F = Q T Q^H by Householder reflections (one warp,
+//                 shuffle reductions, no divisions: fp32 MUFU seeds refined by
+//                 fp64 Newton steps), T made real by a diagonal phase D; all
+//                 eigenvalues of T by multisection (G threads per eigenvalue,
+//                 division-free scaled Sturm counts, ceil(53/log2(G+1)) steps);
+//   trid_vectors: eigenvectors of T for the k largest eigenvalues from the
+//                 leading / trailing Sturm determinants P_i, Q_i (the twisted
+//                 factorisation written without divisions: twist at argmax
+//                 |P_r Q_{r+1}|, z_i ~ prod e * P_i Q_{r+1} resp. prod e *
+//                 Q_{i+1} P_r), modified Gram-Schmidt inside clusters closer
+//                 than 1e-4 ||T||, back-transformation u = Q D z (one warp per
+//                 vector).  Returns false if a cluster vector is numerically
+//                 dependent (caller falls back to Jacobi).
+template <int NMAX>
+struct TridSmem {
+  static constexpr int LD = NMAX + 1;
+  cplx hv[NMAX * LD];        // Householder vector of column k in column k (rows k+1..)
+  cplx w[NMAX];
+  cplx ph[NMAX];             // D = diag(ph)
+  double tau[NMAX];
+  double dg[NMAX];           // diag of T (normalised)
+  double e2[NMAX];           // squared off-diagonal of T
+  double of[NMAX];           // off-diagonal of T
+  double lam[NMAX];          // ascending eigenvalues of T
+  double Z[NMAX * LD];       // real eigenvectors of T (column t <-> eigenvalue n-1-t)
+  double red[32];
+  long long tph[5];          // clock64 per phase (diagnostics)
+  double anrm;
+  int bad;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// full-precision rsqrt / reciprocal from an fp32 MUFU seed (argument must be
+// a normal fp32 number) and fp64 Newton steps
+__device__ __forceinline__ double rsqrt_f64(double x) {
+  if (!(x > 1e-36 && x < 1e36)) return 1.0 / sqrt(x);   // outside the fp32 seed range
+  float xf = (float)x, yf;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(xf));
+  double y = (double)yf;
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+__device__ __forceinline__ double rcp_f64(double x) {
+  const double ax = fabs(x);
+  if (!(ax > 1e-36 && ax < 1e36)) return 1.0 / x;      // outside the fp32 seed range
+  float xf = (float)x, yf;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(yf) : "f"(xf));
+  double y = (double)yf;
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// number of eigenvalues of T below x: sign changes of p_0 = 1,
+// p_i = (dg_i - x) p_{i-1} - e2_{i-1} p_{i-2} (zero on the negative side)
+template <int NMAX>
+__device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const double (&e2)[NMAX], int n, double x) {
+  double p0 = 1.0, p1 = dg[0] - x;
+  int cnt = (p1 <= 0.0);
+#pragma unroll
+  for (int i = 1; i < NMAX; ++i) {
+    if (i < n) {
+      const double p2 = fma(dg[i] - x, p1, -e2[i - 1] * p0);
+      cnt += (p2 <= 0.0) != (p1 <= 0.0);
+      p0 = p1;
+      p1 = p2;
+      if ((i & 7) == 7) {
+        const double a = fabs(p1) + fabs(p0);
+        if (a > 1e120 || a < 1e-120) {
+          const double sc = a > 1e120 ? 1e-120 : 1e120;
+          p0 *= sc;
+          p1 *= sc;
+        }
+      }
+    }
+  }
+  return cnt;
+}
+
+template <int NMAX, int NT>
+__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out) {
+  constexpr int LD = NMAX + 1;
+  const int tid = threadIdx.x, lane = tid & 31;
+  // ---- normalise by ||A||_F
+  double nrm2 = 0.0;
+  for (int e = tid; e < n * n; e += NT) nrm2 += cabs2(A0[(e % n) + LDA * (e / n)]);
+  nrm2 = block_sum<NT>(nrm2, S.red);
+  const double anrm = sqrt(nrm2);
+  const double inv = anrm > 0.0 ? 1.0 / anrm : 1.0;
+  for (int e = tid; e < n * n; e += NT) {
+    const int i = e % n, j = e / n;
+    A0[i + LDA * j] = cscale(A0[i + LDA * j], inv);
+  }
+  if (tid == 0) { S.bad = 0; S.anrm = anrm; }
+  __syncthreads();
+  long long tt0 = clock64();
+  // ---- Householder tridiagonalisation (warp 0; lane = row)
+  if (tid < 32) {
+    for (int k = 0; k + 2 < n; ++k) {
+      const int m = n - k - 1;
+      const int i = k + 1 + lane;
+      const cplx xi = (lane < m) ? A0[i + LDA * k] : czero();
+      const double s2 = warp_sum(cabs2(xi));
+      const cplx x0 = make_double2(__shfl_sync(0xffffffffu, xi.x, 0), __shfl_sync(0xffffffffu, xi.y, 0));
+      if (!(s2 > 1e-60)) {
+        if (lane == 0) S.tau[k] = 0.0;
+        __syncwarp();
+        continue;
+      }
+      const double rs = rsqrt_f64(s2);
+      const double sig = s2 * rs;
+      const double x02 = cabs2(x0);
+      cplx phs = cmk(1.0, 0.0);
+      double ax0 = 0.0;
+      if (x02 > 1e-60) {
+        const double r0 = rsqrt_f64(x02);
+        ax0 = x02 * r0;
+        phs = cscale(x0, r0);
+      }
+      const cplx alpha = cmk(-phs.x * sig, -phs.y * sig);
+      const cplx vi = (lane == 0) ? cscale(phs, ax0 + sig) : xi;
+      const double tau = rcp_f64(sig * (sig + ax0));
+      if (lane < m) S.hv[i + LD * k] = vi;
+      if (lane == 0) S.tau[k] = tau;
+      __syncwarp();
+      // p = tau B v, B = A[k+1.., k+1..]
+      cplx p = czero();
+      if (lane < m) {
+        cplx q0 = czero(), q1 = czero();
+#pragma unroll
+        for (int j = 0; j < NMAX; j += 2) {
+          if (j < m) q0 = cfma(A0[i + LDA * (k + 1 + j)], S.hv[k + 1 + j + LD * k], q0);
+          if (j + 1 < m) q1 = cfma(A0[i + LDA * (k + 2 + j)], S.hv[k + 2 + j + LD * k], q1);
+        }
+        p = cscale(cadd(q0, q1), tau);
+      }
+      const double vp = warp_sum(lane < m ? (vi.x * p.x + vi.y * p.y) : 0.0);
+      const double K = 0.5 * tau * vp;
+      const cplx wi = cmk(p.x - K * vi.x, p.y - K * vi.y);
+      if (lane < m) S.w[lane] = wi;
+      __syncwarp();
+      if (lane < m) {
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+          if (j < m) {
+            const cplx vj = S.hv[k + 1 + j + LD * k], wj = S.w[j];
+            const cplx b = A0[i + LDA * (k + 1 + j)];
+            A0[i + LDA * (k + 1 + j)] = csub(b, cfma_bc(vi, wj, cmul(wi, cconj(vj))));
+          }
+        }
+        A0[i + LDA * k] = (lane == 0) ? alpha : czero();
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      cplx ph = cmk(1.0, 0.0);
+      S.ph[0] = ph;
+      for (int k = 0; k + 1 < n; ++k) {
+        const cplx b = A0[(k + 1) + LDA * k];
+        const double ab2 = cabs2(b);
+        double ab = 0.0;
+        if (ab2 > 1e-60) {
+          const double r = rsqrt_f64(ab2);
+          ab = ab2 * r;
+          ph = cmul(ph, cscale(b, r));
+        }
+        S.ph[k + 1] = ph;
+        S.of[k] = ab;
+        S.e2[k] = ab * ab;
+      }
+    }
+    if (lane < n) S.dg[lane] = A0[lane + LDA * lane].x;
+  }
+  __syncthreads();
+  if (tid == 0) { long long t = clock64(); S.tph[0] = t - tt0; tt0 = t; }
+  // ---- eigenvalues by multisection
+  {
+    double dg[NMAX], e2[NMAX];
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      dg[i] = (i < n) ? S.dg[i] : 0.0;
+      e2[i] = (i + 1 < n) ? S.e2[i] : 0.0;
+    }
+    double lo = 1e300, hi = -1e300;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      if (i < n) {
+        const double r = (i > 0 ? S.of[i - 1] : 0.0) + (i + 1 < n ? S.of[i] : 0.0);
+        lo = fmin(lo, dg[i] - r);
+        hi = fmax(hi, dg[i] + r);
+      }
+    }
+    const double pad = 1e-14 * fmax(1.0, fmax(fabs(lo), fabs(hi)));
+    lo -= pad;
+    hi += pad;
+    const int gl = n <= 8 ? 32 : (n <= 16 ? 16 : 8);      // threads per eigenvalue
+    const int k = tid / gl, j = tid % gl;
+    const int steps = gl == 32 ? 11 : (gl == 16 ? 13 : 17);
+    const double sj = (double)(j + 1) / (double)(gl + 1);
+    const double inv_g1 = 1.0 / (double)(gl + 1);
+    double l = lo, h = hi;
+    const int base = (tid & 31) & ~(gl - 1);
+    const unsigned gmask = (gl == 32) ? 0xffffffffu : (((1u << gl) - 1u) << base);
+    for (int st = 0; st < steps; ++st) {
+      const double x = l + (h - l) * sj;
+      const int c = (k < n) ? sturm_count<NMAX>(dg, e2, n, x) : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, c >= k + 1) & gmask;
+      const int first = bal ? (__ffs(bal) - 1 - base) : gl;
+      const double w = h - l;
+      const double nh = (first < gl) ? l + w * (double)(first + 1) * inv_g1 : h;
+      const double nl = (first > 0) ? l + w * (double)first * inv_g1 : l;
+      l = nl;
+      h = nh;
+    }
+    if (k < n && j == 0) S.lam[k] = 0.5 * (l + h);
+  }
+  __syncthreads();
+  for (int kk = tid; kk < n; kk += NT) lam_out[kk] = S.lam[n - 1 - kk] * anrm;
+  if (tid == 0) { long long t = clock64(); S.tph[1] = t - tt0; }
+  __syncthreads();
+}
+
+template <int NMAX, int NT>
+__device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, cplx* U_out, int LDU) {
+  constexpr int LD = NMAX + 1;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  long long tt0 = clock64();
+  // ---- eigenvectors of T (division-free twisted factorisation), one thread each
+  if (tid < nvec) {
+    const int k = n - 1 - tid;
+    const double lam = S.lam[k];
+    double P[NMAX + 1], Qd[NMAX + 2];
+    double dgl[NMAX], e2[NMAX], of[NMAX];
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      dgl[i] = (i < n) ? S.dg[i] - lam : 0.0;
+      e2[i] = (i + 1 < n) ? S.e2[i] : 0.0;
+      of[i] = (i + 1 < n) ? S.of[i] : 0.0;
+    }
+    // leading determinants P_0..P_n and trailing Q_0..Q_n (Q_n = 1),
+    // rescaled jointly per side to stay in range
+    P[0] = 1.0;
+    P[1] = dgl[0];
+#pragma unroll
+    for (int i = 1; i < NMAX; ++i)
+      if (i < n) P[i + 1] = fma(dgl[i], P[i], -e2[i - 1] * P[i - 1]);
+    Qd[NMAX + 1] = 0.0;
+#pragma unroll
+    for (int i = NMAX; i >= 0; --i) {
+      if (i == n) Qd[i] = 1.0;
+      else if (i == n - 1) Qd[i] = dgl[i];
+      else if (i < n - 1) Qd[i] = fma(dgl[i], Qd[i + 1], -e2[i] * Qd[i + 2]);
+    }
+    // twist r = argmax |P_r Q_{r+1}|
+    int r = 0;
+    double best = -1.0;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      if (i < n) {
+        const double v = fabs(P[i] * Qd[i + 1]);
+        if (v > best) { best = v; r = i; }
+      }
+    }
+    double z[NMAX];
+    // i <= r: z_i = (-1)^{r-i} (prod_{k=i}^{r-1} e_k) P_i Q_{r+1}
+    // i >= r: z_i = (-1)^{i-r} (prod_{k=r}^{i-1} e_k) Q_{i+1} P_r
+    double Qr1 = 0.0, Pr = 0.0;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) if (i == r) { Qr1 = Qd[i + 1]; Pr = P[i]; }
+    double prod = 1.0;
+#pragma unroll
+    for (int i = NMAX - 1; i >= 0; --i) {
+      if (i < n && i <= r) {
+        if (i < r) prod = -prod * of[i];
+        z[i] = prod * P[i] * Qr1;
+      }
+    }
+    prod = 1.0;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      if (i < n && i > r) {
+        prod = -prod * of[i - 1];
+        z[i] = prod * Qd[i + 1] * Pr;
+      }
+    }
+    double nz = 0.0;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) if (i < n) nz = fma(z[i], z[i], nz);
+    const double rn = (nz > 0.0) ? rsqrt_f64(nz) : 0.0;
+    double* zc = S.Z + LD * tid;
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) if (i < n) zc[i] = z[i] * rn;
+    if (!(nz > 0.0)) S.bad = 1;
+  }
+  __syncthreads();
+  if (tid == 0) { long long t = clock64(); S.tph[2] = t - tt0; tt0 = t; }
+  // ---- re-orthogonalise clusters (normalised eigenvalues within 1e-4)
+  if (tid == 0) {
+    int c0 = 0;
+    while (c0 < nvec) {
+      int c1 = c0 + 1;
+      while (c1 < nvec && S.lam[n - 1 - (c1 - 1)] - S.lam[n - 1 - c1] <= 1e-4) ++c1;
+      for (int a = c0 + 1; a < c1; ++a) {
+        double* za = S.Z + LD * a;
+        for (int b = c0; b < a; ++b) {
+          const double* zb = S.Z + LD * b;
+          double d = 0.0;
+          for (int i = 0; i < n; ++i) d += zb[i] * za[i];
+          for (int i = 0; i < n; ++i) za[i] -= d * zb[i];
+        }
+        double nz = 0.0;
+        for (int i = 0; i < n; ++i) nz += za[i] * za[i];
+        if (!(nz > 1e-6)) S.bad = 1;
+        const double rn = 1.0 / sqrt(nz);
+        for (int i = 0; i < n; ++i) za[i] *= rn;
+      }
+      c0 = c1;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) { long long t = clock64(); S.tph[3] = t - tt0; tt0 = t; }
+  if (S.bad) return false;
+  // ---- back-transformation u = Q D z: one warp per vector, lane = row
+  for (int t = wp; t < nvec; t += NT / 32) {
+    const double* z = S.Z + LD * t;
+    cplx u = (lane < n) ? cscale(S.ph[lane], z[lane]) : czero();
+    for (int k = n - 3; k >= 0; --k) {
+      const double tau = S.tau[k];
+      if (tau == 0.0) continue;
+      const cplx v = (lane > k && lane < n) ? S.hv[lane + LD * k] : czero();
+      const cplx c = cfmac(v, u, czero());
+      const double sr = warp_sum(c.x), si = warp_sum(c.y);
+      const cplx s = cmk(sr * tau, si * tau);
+      u = csub(u, cmul(v, s));
+    }
+    if (lane < n) U_out[lane + LDU * t] = u;
+  }
+  __syncthreads();
+  if (tid == 0) S.tph[4] = clock64() - tt0;
+  return true;
+}
+
+template <int NMAX>
+struct EigSmem {
+  static constexpr int LD = NMAX + 1;
+  cplx A[2][NMAX * LD];
+  cplx V[2][NMAX * LD];
+  union {
+    struct {
+      float2 Af[2][NMAX * LD];
+      float2 Vf[2][NMAX * LD];
+    } f;
+    TridSmem<NMAX> tr;
+  } u;
+  JacPar par[NMAX + 1];
+  JacParF parf[NMAX + 1];
+  double lam[NMAX];
+  int rank_of[NMAX];
+  double red[32];
+  int sweeps;
+  int fallbacks;
+  int sweeps32;
+  long long tphase[4];   // clock64 cycles: fp32 sweeps, basis change, fp64 sweeps, sort
+};
+
 
 // ---- fast reciprocal / rsqrt: one MUFU op (fp32 approx) or MUFU + Newton
 // steps to full fp64 precision (no IEEE slow-path subroutine calls)
@@ -265,8 +627,8 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
     int i = e % n, j = e / n;
     const cplx v = E.A[0][i + LD * j];
     nrm2 += cabs2(v);
-    E.Af[0][i + LD * j] = make_float2((float)v.x, (float)v.y);
-    E.Vf[0][i + LD * j] = make_float2(i == j ? 1.f : 0.f, 0.f);
+    E.u.f.Af[0][i + LD * j] = make_float2((float)v.x, (float)v.y);
+    E.u.f.Vf[0][i + LD * j] = make_float2(i == j ? 1.f : 0.f, 0.f);
   }
   nrm2 = block_sum<NT>(nrm2, E.red);     // contains barriers
   long long tc0 = clock64();
@@ -280,7 +642,7 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
     for (; sw < 16 && !conv; ++sw) {
       int any_sweep = 0;
       for (int round = 0; round < N - 1; ++round) {
-        const float2* A = E.Af[cur];
+        const float2* A = E.u.f.Af[cur];
         int did = 0;
         if (tid < half) {
           int p, q;
@@ -317,9 +679,9 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
         }
         if (!__syncthreads_or(did)) continue;
         any_sweep = 1;
-        float2* An = E.Af[cur ^ 1];
-        const float2* V = E.Vf[cur];
-        float2* Vn = E.Vf[cur ^ 1];
+        float2* An = E.u.f.Af[cur ^ 1];
+        const float2* V = E.u.f.Vf[cur];
+        float2* Vn = E.u.f.Vf[cur ^ 1];
         for_elems<NMAX, NT>(n, [&](int i, int j) {
           const JacParF Pi = E.parf[i], Pj = E.parf[j];
           An[i + LD * j] = jac_elem_f(A, LD, i, j, Pi, Pj);
@@ -334,7 +696,7 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
         double off = 0.0;
         for (int e = tid; e < n * n; e += NT) {
           const int i = e % n, j = e / n;
-          if (i != j) { const float2 v = E.Af[cur][i + LD * j]; off += (double)v.x * v.x + (double)v.y * v.y; }
+          if (i != j) { const float2 v = E.u.f.Af[cur][i + LD * j]; off += (double)v.x * v.x + (double)v.y * v.y; }
         }
         off = block_sum<NT>(off, E.red);
         conv = off <= 1e-8 * nrm2;
@@ -345,7 +707,7 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
     // V (fp64) <- Vf; two Newton-Schulz steps V <- V (3 I - V^H V) / 2
     for (int e = tid; e < n * n; e += NT) {
       int i = e % n, j = e / n;
-      const float2 v = E.Vf[cur][i + LD * j];
+      const float2 v = E.u.f.Vf[cur][i + LD * j];
       E.V[0][i + LD * j] = cmk((double)v.x, (double)v.y);
     }
     __syncthreads();
@@ -483,6 +845,45 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
   if (tid == 0) E.tphase[3] = clock64() - tc0;
   if (!conv && tid == 0) raise_status(status, ST_NOCONV);
   return U;
+}
+
+// Two-call eigendecomposition of the Hermitian n x n matrix in E.A[0]:
+//   eig_values(E, n)          -> E.lam (descending, all n);
+//   eig_vectors(E, n, k, st)  -> pointer to the eigenvectors of the k largest
+//                                eigenvalues (column-major, ld NMAX+1).
+// Tridiagonal solver first; Jacobi (whole problem again) if it reports a
+// dependent cluster (status bit ST_FALLBACK).
+template <int NMAX, int NT>
+__device__ void eig_values(EigSmem<NMAX>& E, int n) {
+  constexpr int LD = NMAX + 1;
+  for (int e = threadIdx.x; e < n * n; e += NT) {
+    const int i = e % n, j = e / n;
+    E.A[1][i + LD * j] = E.A[0][i + LD * j];
+  }
+  __syncthreads();
+  trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam);
+}
+
+template <int NMAX, int NT>
+__device__ const cplx* eig_vectors(EigSmem<NMAX>& E, int n, int k, int* status) {
+  constexpr int LD = NMAX + 1;
+  if (k > n) k = n;
+  if (k < 1) k = 1;
+  if (trid_vectors<NMAX, NT>(E.u.tr, n, k, E.V[0], LD)) return E.V[0];
+  for (int e = threadIdx.x; e < n * n; e += NT) {
+    const int i = e % n, j = e / n;
+    E.A[0][i + LD * j] = E.A[1][i + LD * j];
+  }
+  if (threadIdx.x == 0) { E.fallbacks++; raise_status(status, ST_FALLBACK); }
+  __syncthreads();
+  return jacobi_eig<NMAX, NT>(E, n, status);
+}
+
+// one-call form (all k requested vectors), used by the test entry point
+template <int NMAX, int NT>
+__device__ const cplx* eig_small(EigSmem<NMAX>& E, int n, int k, int* status) {
+  eig_values<NMAX, NT>(E, n);
+  return eig_vectors<NMAX, NT>(E, n, k, status);
 }
 
 // --------------------------------------------------------------- RANK rule

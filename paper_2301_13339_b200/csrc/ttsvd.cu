@@ -228,13 +228,14 @@ __global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nb
       S.E.A[0][i + LD * j] = cmk(s, 0.0);
     }
     __syncthreads();
-    const cplx* U = jacobi_eig<32, NT>(S.E, rr, prm.status);
+    eig_values<32, NT>(S.E, rr);
     if (tid == 0) {
       int mp = rr < (1 << (d - k)) ? rr : (1 << (d - k));
       S.rk = rank_rule(S.E.lam, mp, tau2, prm.rmax, prm.ctol);
     }
     __syncthreads();
     const int rk = S.rk;
+    const cplx* U = eig_vectors<32, NT>(S.E, rr, rk, prm.status);
     write_core_from_U(pr, k, U, LD, rr, rk);
     // P_k[a][r] = sum_rho P_{k-1}[a mod h][rho] U[rho + r_prev (a div h)][r]
     double* Pn = S.P[cur ^ 1];
@@ -394,13 +395,14 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
     S.E.A[0][i + LD * j] = cmk(s, 0.0);
   }
   __syncthreads();
-  const cplx* U = jacobi_eig<32, NT>(S.E, rr, prm.status);
+  eig_values<32, NT>(S.E, rr);
   if (tid == 0) {
     int mp = rr < (1 << (pr.d - k)) ? rr : (1 << (pr.d - k));
     S.rk = rank_rule(S.E.lam, mp, *pr.tau2, prm.rmax, prm.ctol);
   }
   __syncthreads();
   const int rk = S.rk;
+  const cplx* U = eig_vectors<32, NT>(S.E, rr, rk, prm.status);
   write_core_from_U(pr, k, U, LD, rr, rk);
   for (int e = tid; e < rr * rk; e += NT) {
     int a = e % rr, r = e / rr;
@@ -486,13 +488,14 @@ __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart,
       S.E.A[0][i + LD * j] = cmk(S.G[i * 32 + j], 0.0);
     }
     __syncthreads();
-    const cplx* U = jacobi_eig<32, NT>(S.E, rr, prm.status);
+    eig_values<32, NT>(S.E, rr);
     if (tid == 0) {
       int mp = rr < n ? rr : n;
       S.rk = rank_rule(S.E.lam, mp, tau2, prm.rmax, prm.ctol);
     }
     __syncthreads();
     const int rk = S.rk;
+    const cplx* U = eig_vectors<32, NT>(S.E, rr, rk, prm.status);
     write_core_from_U(pr, k, U, LD, rr, rk);
     // W_k = U_r^T M_k
     const double* M = S.B[cur];

@@ -39,7 +39,7 @@ class Report(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int), ("ranks_f", ctypes.c_int * 64), ("ranks_g", ctypes.c_int * 64),
                 ("ranks_fh", ctypes.c_int * 64), ("ranks_gh", ctypes.c_int * 64),
                 ("ranks_z", ctypes.c_int * 64), ("ranks_out", ctypes.c_int * 64),
-                ("ms_total", ctypes.c_float)]
+                ("ms_total", ctypes.c_float), ("status_bits", ctypes.c_int)]
 
 
 class QttError(RuntimeError):
@@ -89,7 +89,7 @@ def lib():
     L.qtt_build_info.restype = ctypes.c_char_p
     L.qtt_build_info.argtypes = []
     L.qtt_debug_eigh.restype = I
-    L.qtt_debug_eigh.argtypes = [P, I, P, P, P, I, P]
+    L.qtt_debug_eigh.argtypes = [P, I, P, P, P, I, I, P]
     L.qtt_profile_enable.restype = None
     L.qtt_profile_enable.argtypes = [I]
     L.qtt_profile_read.restype = I
@@ -188,16 +188,18 @@ def qtt_conv_full(f_ptr, g_ptr, y_ptr, shp, dec, fft, shift, scale, ws_ptr, ws_b
         return None
     d = rep.d
     return {"d": d, "ranks_f": list(rep.ranks_f[:d + 1]), "ranks_g": list(rep.ranks_g[:d + 1]),
-            "ranks_out": list(rep.ranks_out[:d + 1]), "ms_total": rep.ms_total}
+            "ranks_out": list(rep.ranks_out[:d + 1]), "ms_total": rep.ms_total,
+            "status_bits": rep.status_bits}
 
 
 def build_info():
     return lib().qtt_build_info().decode()
 
 
-def qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, stream=0, reps=1):
-    """Test-only: the path's CTA Jacobi eigensolver on one Hermitian matrix."""
-    _check(lib().qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, reps, stream))
+def qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, stream=0, reps=1, mode=0):
+    """Test-only: the path's small Hermitian eigensolver on one matrix
+    (mode 0: tridiagonal with Jacobi fallback, as in production; 1: Jacobi)."""
+    _check(lib().qtt_debug_eigh(a_ptr, n, lam_ptr, u_ptr, sweeps_ptr, reps, mode, stream))
 
 
 def qtt_debug_tt_from_host(shp, cores_c128, ranks_i32, rcap, ws_ptr, ws_bytes, stream=0, ws_owner=None):
