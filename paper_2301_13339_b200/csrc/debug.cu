@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(NT) k_debug_eigh(const cplx* A, int n, double*
     sweeps[0] = E.sweeps;
     sweeps[1] = E.fallbacks;
     for (int k = 0; k < 5; ++k) sweeps[2 + k] = (int)E.u.tr.tph[k];
+    for (int k = 0; k < 5; ++k) sweeps[7 + k] = (int)E.u.tr.tstep[k];
   }
 }
 }  // namespace qtt

@@ -170,6 +170,7 @@ struct TridSmem {
   double Z[NMAX * LD];       // real eigenvectors of T (column t <-> eigenvalue n-1-t)
   double red[32];
   long long tph[5];          // clock64 per phase (diagnostics)
+  long long tstep[5];        // clock64 per tridiagonalisation sub-phase (diagnostics)
   double anrm;
   int bad;
 };
@@ -209,12 +210,15 @@ __device__ __forceinline__ double rcp_f64(double x) {
 template <int NMAX>
 __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const double (&e2)[NMAX], int n, double x) {
   double p0 = 1.0, p1 = dg[0] - x;
-  int cnt = (p1 <= 0.0);
+  unsigned s1 = (unsigned)__double2hiint(p1) >> 31;      // sign bits (integer pipe)
+  int cnt = (int)s1;
 #pragma unroll
   for (int i = 1; i < NMAX; ++i) {
     if (i < n) {
       const double p2 = fma(dg[i] - x, p1, -e2[i - 1] * p0);
-      cnt += (p2 <= 0.0) != (p1 <= 0.0);
+      const unsigned s2 = (unsigned)__double2hiint(p2) >> 31;
+      cnt += (int)(s1 ^ s2);
+      s1 = s2;
       p0 = p1;
       p1 = p2;
       if ((i & 7) == 7) {
@@ -228,6 +232,97 @@ __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const doubl
     }
   }
   return cnt;
+}
+
+// Householder tridiagonalisation with the rows in registers (lane i holds row
+// i of the normalised A, n <= NMAX <= 32); all data exchange by shuffles.
+// Writes the reflectors (S.hv, S.tau), D (S.ph) and T (S.dg, S.of, S.e2).
+template <int NMAX>
+__device__ void trid_reduce_regs(TridSmem<NMAX>& S, const cplx* A0, int LDA, int n) {
+  constexpr int LD = NMAX + 1;
+  const int lane = threadIdx.x & 31;
+  cplx a[NMAX];
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) a[j] = (lane < n && j < n) ? A0[lane + LDA * j] : czero();
+#pragma unroll
+  for (int k = 0; k + 2 < NMAX; ++k) {
+    if (k + 2 < n) {
+      const bool act = lane > k && lane < n;
+      const cplx xi = act ? a[k] : czero();
+      const double s2 = warp_sum(cabs2(xi));
+      const cplx x0 = make_double2(__shfl_sync(0xffffffffu, xi.x, k + 1), __shfl_sync(0xffffffffu, xi.y, k + 1));
+      cplx vi = czero();
+      double tau = 0.0;
+      cplx alpha = czero();
+      if (s2 > 1e-60) {
+        const double rs = rsqrt_f64(s2);
+        const double sig = s2 * rs;
+        const double x02 = cabs2(x0);
+        cplx phs = cmk(1.0, 0.0);
+        double ax0 = 0.0;
+        if (x02 > 1e-60) {
+          const double r0 = rsqrt_f64(x02);
+          ax0 = x02 * r0;
+          phs = cscale(x0, r0);
+        }
+        alpha = cmk(-phs.x * sig, -phs.y * sig);
+        vi = (lane == k + 1) ? cscale(phs, ax0 + sig) : xi;
+        tau = rcp_f64(sig * (sig + ax0));
+      }
+      if (act) S.hv[lane + LD * k] = vi;
+      if (lane == 0) S.tau[k] = tau;
+      if (tau != 0.0) {
+        // p_i = tau sum_j a[j] v_j over j = k+1..n-1 (v_j broadcast)
+        cplx q0 = czero(), q1 = czero();
+#pragma unroll
+        for (int j = k + 1; j < NMAX; ++j) {
+          const cplx vj = make_double2(__shfl_sync(0xffffffffu, vi.x, j), __shfl_sync(0xffffffffu, vi.y, j));
+          if (j < n) {
+            if ((j - k) & 1) q0 = cfma(a[j], vj, q0);
+            else q1 = cfma(a[j], vj, q1);
+          }
+        }
+        const cplx p = act ? cscale(cadd(q0, q1), tau) : czero();
+        const double vp = warp_sum(vi.x * p.x + vi.y * p.y);
+        const double K = 0.5 * tau * vp;
+        const cplx wi = cmk(p.x - K * vi.x, p.y - K * vi.y);
+#pragma unroll
+        for (int j = k + 1; j < NMAX; ++j) {
+          const cplx wj = make_double2(__shfl_sync(0xffffffffu, wi.x, j), __shfl_sync(0xffffffffu, wi.y, j));
+          const cplx vj = make_double2(__shfl_sync(0xffffffffu, vi.x, j), __shfl_sync(0xffffffffu, vi.y, j));
+          if (act && j < n) a[j] = csub(a[j], cfma_bc(vi, wj, cmul(wi, cconj(vj))));
+        }
+      }
+      if (act) a[k] = (lane == k + 1) ? alpha : czero();
+    }
+  }
+  // T: diag dg_i = a[i] of lane i, subdiag beta_k = a[k] of lane k+1
+  double dgi = 0.0;
+#pragma unroll
+  for (int j = 0; j < NMAX; ++j) if (j == lane) dgi = a[j].x;
+  cplx bsub = czero();   // lane k+1 holds beta_k in a[k]
+#pragma unroll
+  for (int j = 0; j + 1 < NMAX; ++j) if (j + 1 == lane) bsub = a[j];
+  if (lane < n) S.dg[lane] = dgi;
+  if (lane >= 1 && lane < n) S.w[lane - 1] = bsub;
+  __syncwarp();
+  if (lane == 0) {
+    cplx ph = cmk(1.0, 0.0);
+    S.ph[0] = ph;
+    for (int k = 0; k + 1 < n; ++k) {
+      const cplx b = S.w[k];
+      const double ab2 = cabs2(b);
+      double ab = 0.0;
+      if (ab2 > 1e-60) {
+        const double r = rsqrt_f64(ab2);
+        ab = ab2 * r;
+        ph = cmul(ph, cscale(b, r));
+      }
+      S.ph[k + 1] = ph;
+      S.of[k] = ab;
+      S.e2[k] = ab * ab;
+    }
+  }
 }
 
 template <int NMAX, int NT>
@@ -249,11 +344,14 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   long long tt0 = clock64();
   // ---- Householder tridiagonalisation (warp 0; lane = row)
   if (tid < 32) {
+    long long ts[6] = {0, 0, 0, 0, 0, 0};
+    long long tq = clock64();
     for (int k = 0; k + 2 < n; ++k) {
       const int m = n - k - 1;
       const int i = k + 1 + lane;
       const cplx xi = (lane < m) ? A0[i + LDA * k] : czero();
       const double s2 = warp_sum(cabs2(xi));
+      { long long t = clock64(); ts[0] += t - tq; tq = t; }
       const cplx x0 = make_double2(__shfl_sync(0xffffffffu, xi.x, 0), __shfl_sync(0xffffffffu, xi.y, 0));
       if (!(s2 > 1e-60)) {
         if (lane == 0) S.tau[k] = 0.0;
@@ -276,35 +374,64 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       if (lane < m) S.hv[i + LD * k] = vi;
       if (lane == 0) S.tau[k] = tau;
       __syncwarp();
-      // p = tau B v, B = A[k+1.., k+1..]
+      { long long t = clock64(); ts[1] += t - tq; tq = t; }
+      // p = tau B v, B = A[k+1.., k+1..]; chunks of 8 (loads first)
       cplx p = czero();
       if (lane < m) {
         cplx q0 = czero(), q1 = czero();
 #pragma unroll
-        for (int j = 0; j < NMAX; j += 2) {
-          if (j < m) q0 = cfma(A0[i + LDA * (k + 1 + j)], S.hv[k + 1 + j + LD * k], q0);
-          if (j + 1 < m) q1 = cfma(A0[i + LDA * (k + 2 + j)], S.hv[k + 2 + j + LD * k], q1);
+        for (int j0 = 0; j0 < NMAX; j0 += 8) {
+          if (j0 < m) {
+            cplx bb[8], vv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = j0 + u;
+              const bool ok = j < m;
+              bb[u] = ok ? A0[i + LDA * (k + 1 + j)] : czero();
+              vv[u] = ok ? S.hv[k + 1 + j + LD * k] : czero();
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              q0 = cfma(bb[u], vv[u], q0);
+              q1 = cfma(bb[u + 1], vv[u + 1], q1);
+            }
+          }
         }
         p = cscale(cadd(q0, q1), tau);
       }
+      { long long t = clock64(); ts[2] += t - tq; tq = t; }
       const double vp = warp_sum(lane < m ? (vi.x * p.x + vi.y * p.y) : 0.0);
       const double K = 0.5 * tau * vp;
       const cplx wi = cmk(p.x - K * vi.x, p.y - K * vi.y);
       if (lane < m) S.w[lane] = wi;
       __syncwarp();
+      { long long t = clock64(); ts[3] += t - tq; tq = t; }
       if (lane < m) {
 #pragma unroll
-        for (int j = 0; j < NMAX; ++j) {
-          if (j < m) {
-            const cplx vj = S.hv[k + 1 + j + LD * k], wj = S.w[j];
-            const cplx b = A0[i + LDA * (k + 1 + j)];
-            A0[i + LDA * (k + 1 + j)] = csub(b, cfma_bc(vi, wj, cmul(wi, cconj(vj))));
+        for (int j0 = 0; j0 < NMAX; j0 += 8) {
+          if (j0 < m) {
+            cplx bb[8], vv[8], ww[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = j0 + u;
+              const bool ok = j < m;
+              bb[u] = ok ? A0[i + LDA * (k + 1 + j)] : czero();
+              vv[u] = ok ? S.hv[k + 1 + j + LD * k] : czero();
+              ww[u] = ok ? S.w[j] : czero();
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = j0 + u;
+              if (j < m) A0[i + LDA * (k + 1 + j)] = csub(bb[u], cfma_bc(vi, ww[u], cmul(wi, cconj(vv[u]))));
+            }
           }
         }
         A0[i + LDA * k] = (lane == 0) ? alpha : czero();
       }
       __syncwarp();
+      { long long t = clock64(); ts[4] += t - tq; tq = t; }
     }
+    if (lane == 0) for (int q = 0; q < 5; ++q) S.tstep[q] = ts[q];
     if (lane == 0) {
       cplx ph = cmk(1.0, 0.0);
       S.ph[0] = ph;

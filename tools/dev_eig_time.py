@@ -14,7 +14,7 @@ for mode in (0, 1):
     A = mk(n, rank, dec, pairs=pairs)
     a = torch.from_numpy(np.ascontiguousarray(A.T).view(np.float64).copy()).cuda()
     lam = torch.empty(n, dtype=torch.float64, device='cuda'); U = torch.empty(2*n*n, dtype=torch.float64, device='cuda')
-    sw = torch.zeros(8, dtype=torch.int32, device='cuda')
+    sw = torch.zeros(16, dtype=torch.int32, device='cuda')
     s = torch.cuda.current_stream().cuda_stream
     for _ in range(3): Q.qtt_debug_eigh(a.data_ptr(), n, lam.data_ptr(), U.data_ptr(), sw.data_ptr(), s, mode=mode)
     torch.cuda.synchronize()
@@ -23,4 +23,4 @@ for mode in (0, 1):
     Q.qtt_debug_eigh(a.data_ptr(), n, lam.data_ptr(), U.data_ptr(), sw.data_ptr(), s, reps=50, mode=mode)
     e1.record(); torch.cuda.synchronize()
     v = sw.cpu().numpy()
-    print(f"mode={mode} n={n} rank={rank} decades={dec} pairs={pairs}: {e0.elapsed_time(e1)/50*1000:.1f} us/eig, sweeps={v[0]} fallbacks={v[1]} trid cycles={list(v[2:7])}")
+    print(f"mode={mode} n={n} rank={rank} decades={dec} pairs={pairs}: {e0.elapsed_time(e1)/50*1000:.1f} us/eig, sweeps={v[0]} fallbacks={v[1]} trid cycles={list(v[2:7])} tridiag sub-phases(norm, reflector, matvec, dot+w, update)={list(v[7:12])}")
