@@ -342,96 +342,83 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   if (tid == 0) { S.bad = 0; S.anrm = anrm; }
   __syncthreads();
   long long tt0 = clock64();
-  // ---- Householder tridiagonalisation (warp 0; lane = row)
-  if (tid < 32) {
-    long long ts[6] = {0, 0, 0, 0, 0, 0};
-    long long tq = clock64();
-    for (int k = 0; k + 2 < n; ++k) {
-      const int m = n - k - 1;
+  // ---- Householder tridiagonalisation.  Per step: warp 0 forms the
+  //      reflector; the whole CTA does the matvec p = tau B v (8 threads per
+  //      row, shuffle reduction) and the rank-2 update (one element each).
+  for (int k = 0; k + 2 < n; ++k) {
+    const int m = n - k - 1;
+    if (tid < 32) {
       const int i = k + 1 + lane;
       const cplx xi = (lane < m) ? A0[i + LDA * k] : czero();
       const double s2 = warp_sum(cabs2(xi));
-      { long long t = clock64(); ts[0] += t - tq; tq = t; }
       const cplx x0 = make_double2(__shfl_sync(0xffffffffu, xi.x, 0), __shfl_sync(0xffffffffu, xi.y, 0));
-      if (!(s2 > 1e-60)) {
-        if (lane == 0) S.tau[k] = 0.0;
-        __syncwarp();
-        continue;
-      }
-      const double rs = rsqrt_f64(s2);
-      const double sig = s2 * rs;
-      const double x02 = cabs2(x0);
-      cplx phs = cmk(1.0, 0.0);
-      double ax0 = 0.0;
-      if (x02 > 1e-60) {
-        const double r0 = rsqrt_f64(x02);
-        ax0 = x02 * r0;
-        phs = cscale(x0, r0);
-      }
-      const cplx alpha = cmk(-phs.x * sig, -phs.y * sig);
-      const cplx vi = (lane == 0) ? cscale(phs, ax0 + sig) : xi;
-      const double tau = rcp_f64(sig * (sig + ax0));
-      if (lane < m) S.hv[i + LD * k] = vi;
-      if (lane == 0) S.tau[k] = tau;
-      __syncwarp();
-      { long long t = clock64(); ts[1] += t - tq; tq = t; }
-      // p = tau B v, B = A[k+1.., k+1..]; chunks of 8 (loads first)
-      cplx p = czero();
-      if (lane < m) {
-        cplx q0 = czero(), q1 = czero();
-#pragma unroll
-        for (int j0 = 0; j0 < NMAX; j0 += 8) {
-          if (j0 < m) {
-            cplx bb[8], vv[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = j0 + u;
-              const bool ok = j < m;
-              bb[u] = ok ? A0[i + LDA * (k + 1 + j)] : czero();
-              vv[u] = ok ? S.hv[k + 1 + j + LD * k] : czero();
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u += 2) {
-              q0 = cfma(bb[u], vv[u], q0);
-              q1 = cfma(bb[u + 1], vv[u + 1], q1);
-            }
-          }
+      double tau = 0.0;
+      cplx vi = czero(), alpha = czero();
+      if (s2 > 1e-60) {
+        const double rs = rsqrt_f64(s2);
+        const double sig = s2 * rs;
+        const double x02 = cabs2(x0);
+        cplx phs = cmk(1.0, 0.0);
+        double ax0 = 0.0;
+        if (x02 > 1e-60) {
+          const double r0 = rsqrt_f64(x02);
+          ax0 = x02 * r0;
+          phs = cscale(x0, r0);
         }
-        p = cscale(cadd(q0, q1), tau);
+        alpha = cmk(-phs.x * sig, -phs.y * sig);
+        vi = (lane == 0) ? cscale(phs, ax0 + sig) : xi;
+        tau = rcp_f64(sig * (sig + ax0));
       }
-      { long long t = clock64(); ts[2] += t - tq; tq = t; }
-      const double vp = warp_sum(lane < m ? (vi.x * p.x + vi.y * p.y) : 0.0);
-      const double K = 0.5 * tau * vp;
-      const cplx wi = cmk(p.x - K * vi.x, p.y - K * vi.y);
-      if (lane < m) S.w[lane] = wi;
-      __syncwarp();
-      { long long t = clock64(); ts[3] += t - tq; tq = t; }
       if (lane < m) {
-#pragma unroll
-        for (int j0 = 0; j0 < NMAX; j0 += 8) {
-          if (j0 < m) {
-            cplx bb[8], vv[8], ww[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = j0 + u;
-              const bool ok = j < m;
-              bb[u] = ok ? A0[i + LDA * (k + 1 + j)] : czero();
-              vv[u] = ok ? S.hv[k + 1 + j + LD * k] : czero();
-              ww[u] = ok ? S.w[j] : czero();
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int j = j0 + u;
-              if (j < m) A0[i + LDA * (k + 1 + j)] = csub(bb[u], cfma_bc(vi, ww[u], cmul(wi, cconj(vv[u]))));
-            }
-          }
-        }
+        S.hv[i + LD * k] = vi;
         A0[i + LDA * k] = (lane == 0) ? alpha : czero();
       }
-      __syncwarp();
-      { long long t = clock64(); ts[4] += t - tq; tq = t; }
+      if (lane == 0) S.tau[k] = tau;
     }
-    if (lane == 0) for (int q = 0; q < 5; ++q) S.tstep[q] = ts[q];
+    __syncthreads();
+    const double tau = S.tau[k];
+    if (tau != 0.0) {
+      // p_r = tau sum_j B[r][j] v_j, rows r < m: 8 threads per row
+      {
+        const int r = tid >> 3, part = tid & 7;
+        cplx q = czero();
+        if (r < m) {
+#pragma unroll
+          for (int u = 0; u < (NMAX + 7) / 8; ++u) {
+            const int j = part + 8 * u;
+            if (j < m) q = cfma(A0[(k + 1 + r) + LDA * (k + 1 + j)], S.hv[k + 1 + j + LD * k], q);
+          }
+        }
+        q.x += __shfl_xor_sync(0xffffffffu, q.x, 1);
+        q.y += __shfl_xor_sync(0xffffffffu, q.y, 1);
+        q.x += __shfl_xor_sync(0xffffffffu, q.x, 2);
+        q.y += __shfl_xor_sync(0xffffffffu, q.y, 2);
+        q.x += __shfl_xor_sync(0xffffffffu, q.x, 4);
+        q.y += __shfl_xor_sync(0xffffffffu, q.y, 4);
+        if (r < m && part == 0) S.w[r] = cscale(q, tau);
+      }
+      __syncthreads();
+      // K = (tau/2) Re(v^H p); w = p - K v (warp 0)
+      if (tid < 32) {
+        const cplx pi = (lane < m) ? S.w[lane] : czero();
+        const cplx vi = (lane < m) ? S.hv[k + 1 + lane + LD * k] : czero();
+        const double vp = warp_sum(vi.x * pi.x + vi.y * pi.y);
+        const double K = 0.5 * tau * vp;
+        if (lane < m) S.w[lane] = cmk(pi.x - K * vi.x, pi.y - K * vi.y);
+      }
+      __syncthreads();
+      // B -= v w^H + w v^H, one element per thread
+      for (int e = tid; e < m * m; e += NT) {
+        const int r = e % m, c = e / m;
+        const cplx vr = S.hv[k + 1 + r + LD * k], vc = S.hv[k + 1 + c + LD * k];
+        const cplx wr = S.w[r], wc = S.w[c];
+        cplx* b = &A0[(k + 1 + r) + LDA * (k + 1 + c)];
+        *b = csub(*b, cfma_bc(vr, wc, cmul(wr, cconj(vc))));
+      }
+      __syncthreads();
+    }
+  }
+  if (tid < 32) {
     if (lane == 0) {
       cplx ph = cmk(1.0, 0.0);
       S.ph[0] = ph;
@@ -608,9 +595,13 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, cplx* U_out, in
       const double tau = S.tau[k];
       if (tau == 0.0) continue;
       const cplx v = (lane > k && lane < n) ? S.hv[lane + LD * k] : czero();
-      const cplx c = cfmac(v, u, czero());
-      const double sr = warp_sum(c.x), si = warp_sum(c.y);
-      const cplx s = cmk(sr * tau, si * tau);
+      cplx c = cfmac(v, u, czero());
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        c.x += __shfl_xor_sync(0xffffffffu, c.x, o);
+        c.y += __shfl_xor_sync(0xffffffffu, c.y, o);
+      }
+      const cplx s = cmk(c.x * tau, c.y * tau);
       u = csub(u, cmul(v, s));
     }
     if (lane < n) U_out[lane + LDU * t] = u;
