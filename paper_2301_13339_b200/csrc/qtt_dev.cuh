@@ -207,28 +207,28 @@ __device__ __forceinline__ double rcp_f64(double x) {
 
 // number of eigenvalues of T below x: sign changes of p_0 = 1,
 // p_i = (dg_i - x) p_{i-1} - e2_{i-1} p_{i-2} (zero on the negative side)
+// T is padded to NMAX with decoupled diagonal entries 4.0 (above the spectrum
+// of the normalised T, |lambda| <= ||T||_F = 1) so every loop runs
+// unpredicated: the padding adds no sign change for x < 4 and no eigenvector
+// component.
 template <int NMAX>
-__device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const double (&e2)[NMAX], int n, double x) {
+__device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const double (&e2)[NMAX], double x) {
   double p0 = 1.0, p1 = dg[0] - x;
   unsigned s1 = (unsigned)__double2hiint(p1) >> 31;      // sign bits (integer pipe)
   int cnt = (int)s1;
 #pragma unroll
   for (int i = 1; i < NMAX; ++i) {
-    if (i < n) {
-      const double p2 = fma(dg[i] - x, p1, -e2[i - 1] * p0);
-      const unsigned s2 = (unsigned)__double2hiint(p2) >> 31;
-      cnt += (int)(s1 ^ s2);
-      s1 = s2;
-      p0 = p1;
-      p1 = p2;
-      if ((i & 7) == 7) {
-        const double a = fabs(p1) + fabs(p0);
-        if (a > 1e120 || a < 1e-120) {
-          const double sc = a > 1e120 ? 1e-120 : 1e120;
-          p0 *= sc;
-          p1 *= sc;
-        }
-      }
+    const double p2 = fma(dg[i] - x, p1, -e2[i - 1] * p0);
+    const unsigned s2 = (unsigned)__double2hiint(p2) >> 31;
+    cnt += (int)(s1 ^ s2);
+    s1 = s2;
+    p0 = p1;
+    p1 = p2;
+    if ((i & 7) == 7 && i + 1 < NMAX) {
+      const double a = fabs(p1) + fabs(p0);
+      const double sc = a > 1e120 ? 1e-120 : (a < 1e-120 ? 1e120 : 1.0);
+      p0 *= sc;
+      p1 *= sc;
     }
   }
   return cnt;
@@ -445,7 +445,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     double dg[NMAX], e2[NMAX];
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) {
-      dg[i] = (i < n) ? S.dg[i] : 0.0;
+      dg[i] = (i < n) ? S.dg[i] : 4.0;
       e2[i] = (i + 1 < n) ? S.e2[i] : 0.0;
     }
     double lo = 1e300, hi = -1e300;
@@ -470,7 +470,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     const unsigned gmask = (gl == 32) ? 0xffffffffu : (((1u << gl) - 1u) << base);
     for (int st = 0; st < steps; ++st) {
       const double x = l + (h - l) * sj;
-      const int c = (k < n) ? sturm_count<NMAX>(dg, e2, n, x) : 0;
+      const int c = (k < n) ? sturm_count<NMAX>(dg, e2, x) : 0;
       const unsigned bal = __ballot_sync(0xffffffffu, c >= k + 1) & gmask;
       const int first = bal ? (__ffs(bal) - 1 - base) : gl;
       const double w = h - l;
@@ -500,59 +500,51 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, cplx* U_out, in
     double dgl[NMAX], e2[NMAX], of[NMAX];
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) {
-      dgl[i] = (i < n) ? S.dg[i] - lam : 0.0;
+      dgl[i] = (i < n) ? S.dg[i] - lam : 4.0 - lam;
       e2[i] = (i + 1 < n) ? S.e2[i] : 0.0;
       of[i] = (i + 1 < n) ? S.of[i] : 0.0;
     }
-    // leading determinants P_0..P_n and trailing Q_0..Q_n (Q_n = 1),
-    // rescaled jointly per side to stay in range
+    // leading determinants P_0..P_NMAX and trailing Q_0..Q_NMAX (Q_NMAX = 1)
     P[0] = 1.0;
     P[1] = dgl[0];
 #pragma unroll
-    for (int i = 1; i < NMAX; ++i)
-      if (i < n) P[i + 1] = fma(dgl[i], P[i], -e2[i - 1] * P[i - 1]);
+    for (int i = 1; i < NMAX; ++i) P[i + 1] = fma(dgl[i], P[i], -e2[i - 1] * P[i - 1]);
     Qd[NMAX + 1] = 0.0;
+    Qd[NMAX] = 1.0;
+    Qd[NMAX - 1] = dgl[NMAX - 1];
 #pragma unroll
-    for (int i = NMAX; i >= 0; --i) {
-      if (i == n) Qd[i] = 1.0;
-      else if (i == n - 1) Qd[i] = dgl[i];
-      else if (i < n - 1) Qd[i] = fma(dgl[i], Qd[i + 1], -e2[i] * Qd[i + 2]);
-    }
-    // twist r = argmax |P_r Q_{r+1}|
+    for (int i = NMAX - 2; i >= 0; --i) Qd[i] = fma(dgl[i], Qd[i + 1], -e2[i] * Qd[i + 2]);
+    // twist r = argmax_{i < n} |P_i Q_{i+1}|
     int r = 0;
     double best = -1.0;
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) {
-      if (i < n) {
-        const double v = fabs(P[i] * Qd[i + 1]);
-        if (v > best) { best = v; r = i; }
-      }
+      const double v = (i < n) ? fabs(P[i] * Qd[i + 1]) : -2.0;
+      if (v > best) { best = v; r = i; }
     }
     double z[NMAX];
     // i <= r: z_i = (-1)^{r-i} (prod_{k=i}^{r-1} e_k) P_i Q_{r+1}
-    // i >= r: z_i = (-1)^{i-r} (prod_{k=r}^{i-1} e_k) Q_{i+1} P_r
+    // i >= r: z_i = (-1)^{i-r} (prod_{k=r}^{i-1} e_k) Q_{i+1} P_r   (e_{n-1..} = 0)
     double Qr1 = 0.0, Pr = 0.0;
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) if (i == r) { Qr1 = Qd[i + 1]; Pr = P[i]; }
     double prod = 1.0;
 #pragma unroll
     for (int i = NMAX - 1; i >= 0; --i) {
-      if (i < n && i <= r) {
-        if (i < r) prod = -prod * of[i];
-        z[i] = prod * P[i] * Qr1;
-      }
+      if (i < r) prod = -prod * of[i];
+      z[i] = (i <= r) ? prod * P[i] * Qr1 : 0.0;
     }
     prod = 1.0;
 #pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
-      if (i < n && i > r) {
+    for (int i = 1; i < NMAX; ++i) {
+      if (i > r) {
         prod = -prod * of[i - 1];
         z[i] = prod * Qd[i + 1] * Pr;
       }
     }
     double nz = 0.0;
 #pragma unroll
-    for (int i = 0; i < NMAX; ++i) if (i < n) nz = fma(z[i], z[i], nz);
+    for (int i = 0; i < NMAX; ++i) nz = fma(z[i], z[i], nz);
     const double rn = (nz > 0.0) ? rsqrt_f64(nz) : 0.0;
     double* zc = S.Z + LD * tid;
 #pragma unroll
