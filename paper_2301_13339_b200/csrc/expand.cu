@@ -4,19 +4,19 @@
 //
 // y[i] = Re(C_1[i_1] ... C_d[i_d]).  The chain is split at m_e = 8:
 //   L = full(cores 1..8)  (256 x r, complex)          k_expand_prep
-//   R = full(cores 9..d)  (r x 2^{d-8}), formed per 4096-element chunk from a
-//       suffix stack of the top cores and a 4-level tree of the mid cores
-//   y_chunk = [Re L, -Im L] (256 x 2r) . [Re R; Im R] (2r x 16)
-// on FP64 tensor cores (DMMA), staged through shared memory so every store is
-// a coalesced 16-byte write (the pass is bound by HBM writes).
+//   R = full(cores 9..d)  (r x 2^{d-8}), formed per 32768-element super-chunk
+//       from a suffix stack of the top cores and a 7-level tree of the mid
+//       cores
+//   y_tile = [Re L, -Im L] (256 x 2r) . [Re R; Im R] (2r x 128)
+// on FP64 tensor cores (DMMA); each accumulator fragment is stored directly
+// (8 consecutive QTT indices per column = whole 32-byte sectors in both
+// layouts, streaming stores) — the pass is bound by HBM writes.
 #include "qtt_kernels.h"
 
 namespace qtt {
 
 static constexpr int NT = 256;
 static constexpr int ME = 8;        // bits of L
-static constexpr int CHX = 4096;    // chunk (64 x 64 square in 2D)
-static constexpr int OSLD = 68;     // staging row stride (interleaved)
 
 // ----------------------------------------------------------- small d
 __global__ void k_expand_small(const ExProb* probs, ExParams P) {
@@ -92,27 +92,34 @@ __global__ void k_expand_prep(const ExProb* probs, ExParams P) {
 }
 
 // ------------------------------------------------------------- main
+// A super-chunk is 2^(ME+MB) consecutive QTT indices: 256 rows (bits 1..8,
+// L) x 128 columns (bits 9..15, the mid tree); the top bits (cores 16..d)
+// are fixed per super-chunk and come from an incrementally updated suffix
+// stack.  Requires d >= ME + MB = 15.
+static constexpr int MB = 7;                 // mid bits
+static constexpr int NCOL = 1 << MB;         // 128 R columns per super-chunk
+static constexpr int TOP0 = ME + MB + 1;     // first top core (15)
+static constexpr int RSLD = NCOL + 4;        // ld of Rs rows (columns + pad)
+
 struct ExSmem {
-  double stage[64 * OSLD];
-  double Rs[32 * 20];         // [Re R; Im R] (KL x 16), ld KLD
-  cplx stack[MAXD][RC];       // suffix products S_k (k = 13..d)
-  cplx tree[2][16 * RC];
+  double Rs[32 * RSLD];       // [Re R; Im R] (KL x 64), row-major, ld RSLD
+  cplx stack[MAXD + 1][RC];   // stack[k-1] = C_k ... C_d (vector of size r_{k-1})
+  cplx tree[2][NCOL * RC];
 };
 
-__global__ void __launch_bounds__(NT) k_expand_main(const ExProb* probs, ExParams P, int per_cta) {
+__global__ void __launch_bounds__(NT, 2) k_expand_main(const ExProb* probs, ExParams P, int per_cta) {
   const ExProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
   ExSmem& S = *reinterpret_cast<ExSmem*>(smraw);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int d = P.d;
-  const uint64_t nchunks = 1ull << (d - 12);
+  const uint64_t nsup = 1ull << (d - ME - MB);
   const uint64_t c0 = (uint64_t)blockIdx.x * per_cta;
   uint64_t c1 = c0 + per_cta;
-  if (c1 > nchunks) c1 = nchunks;
+  if (c1 > nsup) c1 = nsup;
   if (c0 >= c1) return;
   const int r8 = pr.ranks[ME];
   const int kl = (2 * r8 + 3) & ~3;
-  const int kld = (kl % 8 == 0) ? kl + 4 : kl;
   const int ksteps = kl / 4;
   // A fragments: this warp's 4 m-blocks (rows 32 w .. 32 w + 31), all k-steps
   double afr[4][8];
@@ -123,25 +130,28 @@ __global__ void __launch_bounds__(NT) k_expand_main(const ExProb* probs, ExParam
       int row = 32 * w + 8 * mb + (lane >> 2), col = 4 * ks + (lane & 3);
       afr[mb][ks] = (col < kl) ? pr.lsplit[row + 256 * col] : 0.0;
     }
+  if (tid < RC) S.stack[d][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
+  uint32_t offrow[4], offcol[2];
+#pragma unroll
+  for (int mb = 0; mb < 4; ++mb) offrow[mb] = (uint32_t)qtt_offset(32 * w + 8 * mb + (lane >> 2), P.layout, P.bx);
+#pragma unroll
+  for (int e = 0; e < 2; ++e) offcol[e] = (uint32_t)qtt_offset((uint64_t)(2 * (lane & 3) + e) << ME, P.layout, P.bx);
   uint64_t prev = ~0ull;
   for (uint64_t c = c0; c < c1; ++c) {
-    // ---- suffix stack of the top cores 13..d for the bits of c
-    int hi;   // highest core index whose bit changed (>= 13)
+    // ---- suffix stack over the top cores TOP0..d for the bits of c
+    int hi;
     if (prev == ~0ull) hi = d;
-    else {
-      uint64_t diff = prev ^ c;
-      hi = 12 + (64 - __clzll((long long)diff));
-    }
+    else hi = TOP0 - 1 + (64 - __clzll((long long)(prev ^ c)));
+    if (hi > d) hi = d;
+    __syncthreads();
     if (w == 0) {
-      for (int k = hi; k >= 13; --k) {
+      for (int k = hi; k >= TOP0; --k) {
         const int r0 = pr.ranks[k - 1], r1 = pr.ranks[k];
-        const int be = (int)((c >> (k - 13)) & 1);
+        const int be = (int)((c >> (k - TOP0)) & 1);
         const cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
         if (lane < r0) {
           cplx s = czero();
-          if (k == d) s = core[lane + r0 * be];
-          else
-            for (int j = 0; j < r1; ++j) s = cfma(core[lane + r0 * be + 2 * r0 * j], S.stack[k][j], s);
+          for (int j = 0; j < r1; ++j) s = cfma(core[lane + r0 * be + 2 * r0 * j], S.stack[k][j], s);
           S.stack[k - 1][lane] = s;
         }
         __syncwarp();
@@ -149,81 +159,64 @@ __global__ void __launch_bounds__(NT) k_expand_main(const ExProb* probs, ExParam
     }
     prev = c;
     __syncthreads();
-    // ---- mid tree over cores 12, 11, 10, 9 -> 16 vectors of size r_8
-    {
-      const cplx* vin = S.stack[12];
-      int nv = 1;
-      int cur = 0;
-      for (int k = 12; k >= 9; --k) {
-        const int r0 = pr.ranks[k - 1], r1 = pr.ranks[k];
-        const cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
-        cplx* vout = S.tree[cur];
-        // output vector v' = 2*v + be (bit k-9 of the column index is the MSB so far)
-        for (int e = tid; e < 2 * nv * r0; e += NT) {
-          int i = e % r0, vv = e / r0;
-          int be = vv & 1, src = vv >> 1;
-          cplx s = czero();
-          for (int j = 0; j < r1; ++j) s = cfma(core[i + r0 * be + 2 * r0 * j], vin[src * RC + j], s);
-          vout[vv * RC + i] = s;
+    // ---- mid tree over cores ME+MB .. ME+1 -> 64 vectors of size r_8
+    const cplx* vin = S.stack[TOP0 - 1];
+    int nv = 1, cur = 0;
+#pragma unroll 1
+    for (int k = ME + MB; k >= ME + 1; --k) {
+      const int r0 = pr.ranks[k - 1], r1 = pr.ranks[k];
+      const cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
+      cplx* vout = S.tree[cur];
+      for (int e = tid; e < 2 * nv * r0; e += NT) {
+        const int i = e % r0, vv = e / r0;
+        const int be = vv & 1, src = vv >> 1;
+        cplx s0 = czero(), s1 = czero();
+#pragma unroll
+        for (int j = 0; j < RC; j += 2) {
+          if (j < r1) s0 = cfma(core[i + r0 * be + 2 * r0 * j], vin[src * RC + j], s0);
+          if (j + 1 < r1) s1 = cfma(core[i + r0 * be + 2 * r0 * (j + 1)], vin[src * RC + j + 1], s1);
         }
-        __syncthreads();
-        vin = vout;
-        cur ^= 1;
-        nv *= 2;
+        vout[vv * RC + i] = cadd(s0, s1);
       }
-      // vin holds 16 vectors; vector index vv has bits (b12 b11 b10 b9) with b9 as LSB
-      for (int e = tid; e < kl * 16; e += NT) {
-        int row = e % kl, col = e / kl;
-        double v = 0.0;
-        if (row < r8) v = vin[col * RC + row].x;
-        else if (row < 2 * r8) v = vin[col * RC + row - r8].y;
-        S.Rs[row + kld * col] = v;
-      }
+      __syncthreads();
+      vin = vout;
+      cur ^= 1;
+      nv *= 2;
+    }
+    // vector index vv: bits (b_{ME+MB} .. b_{ME+1}), b_{ME+1} the LSB
+    for (int e = tid; e < kl * NCOL; e += NT) {
+      const int row = e / NCOL, col = e % NCOL;
+      double v = 0.0;
+      if (row < r8) v = vin[col * RC + row].x;
+      else if (row < 2 * r8) v = vin[col * RC + row - r8].y;
+      S.Rs[row * RSLD + col] = v;
     }
     __syncthreads();
-    // ---- GEMM: rows 32 w .. +31, 16 columns
-#pragma unroll
-    for (int nb = 0; nb < 2; ++nb) {
+    // ---- GEMM (256 x 128) and direct stores from the fragments.  The layout
+    //      offset is additive over disjoint QTT bit fields: base (bits >= 15)
+    //      + row (bits 0..7) + column block nb (bits 11..14) + column in
+    //      block (bits 8..10), all precomputed outside the inner loop.
+    const uint64_t qbase = c << (ME + MB);
+    double* ybase = pr.y + qtt_offset(qbase, P.layout, P.bx);
+#pragma unroll 1
+    for (int nb = 0; nb < NCOL / 8; ++nb) {
+      const uint32_t offnb = (uint32_t)qtt_offset((uint64_t)(8 * nb) << ME, P.layout, P.bx);
       double acc[4][2];
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < 8; ++ks) {
         if (ks < ksteps) {
-          double b = S.Rs[(4 * ks + (lane & 3)) + kld * (8 * nb + (lane >> 2))];
+          const double bb = S.Rs[(4 * ks + (lane & 3)) * RSLD + 8 * nb + (lane >> 2)];
 #pragma unroll
-          for (int mb = 0; mb < 4; ++mb) dmma884(acc[mb][0], acc[mb][1], afr[mb][ks], b);
+          for (int mb = 0; mb < 4; ++mb) dmma884(acc[mb][0], acc[mb][1], afr[mb][ks], bb);
         }
       }
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          uint32_t row = 32 * w + 8 * mb + (lane >> 2);
-          uint32_t col = 8 * nb + 2 * (lane & 3) + e;
-          uint32_t q = row + (col << ME);
-          int off = (P.layout == LAYOUT_INTERLEAVED)
-                        ? (int)(compact_even(q) + OSLD * compact_even(q >> 1))
-                        : (int)q;
-          S.stage[off] = acc[mb][e];
-        }
+        for (int e = 0; e < 2; ++e) __stcs(ybase + (offrow[mb] + offcol[e] + offnb), acc[mb][e]);
     }
-    __syncthreads();
-    // ---- coalesced store of the chunk
-    if (P.layout == LAYOUT_INTERLEAVED) {
-      const uint64_t q0 = c * (uint64_t)CHX;
-      const uint64_t x0 = compact_even(q0), y0 = compact_even(q0 >> 1);
-      for (int u = tid; u < CHX / 2; u += NT) {
-        int row = u >> 5, cp = u & 31;
-        double2 v = make_double2(S.stage[row * OSLD + 2 * cp], S.stage[row * OSLD + 2 * cp + 1]);
-        *reinterpret_cast<double2*>(pr.y + ((y0 + row) << P.bx) + x0 + 2 * cp) = v;
-      }
-    } else {
-      double* o = pr.y + c * (uint64_t)CHX;
-      for (int u = tid; u < CHX / 2; u += NT)
-        reinterpret_cast<double2*>(o)[u] = reinterpret_cast<const double2*>(S.stage)[u];
-    }
-    __syncthreads();
   }
 }
 
@@ -238,17 +231,19 @@ cudaError_t setup_expand_kernels() {
 
 cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& prm, cudaStream_t st) {
   const int d = prm.d;
-  if (d <= 13) {
+  if (d < ME + MB) {
     int nb = (int)(((1ull << d) + 255) / 256);
     k_expand_small<<<dim3(nb, nprob), 256, 0, st>>>(probs_dev, prm);
     count_launches(1);
     return cudaGetLastError();
   }
   k_expand_prep<<<nprob, 256, PREP_SMEM, st>>>(probs_dev, prm);
-  const uint64_t nchunks = 1ull << (d - 12);
-  const int target = NBLK_MAX;
-  int per = (int)((nchunks + target - 1) / target);
-  int nb = (int)((nchunks + per - 1) / per);
+  const uint64_t nsup = 1ull << (d - ME - MB);
+  // aim for >= 2 CTAs per SM over all problems, contiguous ranges per CTA
+  uint64_t target = (uint64_t)(2 * NBLK_MAX + nprob - 1) / nprob;
+  if (target < 1) target = 1;
+  int per = (int)((nsup + target - 1) / target);
+  int nb = (int)((nsup + per - 1) / per);
   k_expand_main<<<dim3(nb, nprob), NT, sizeof(ExSmem), st>>>(probs_dev, prm, per);
   count_launches(2);
   return cudaGetLastError();
