@@ -320,6 +320,7 @@ def run_ours(a):
         "hbm_passes": passes,
         "clocks": clk.summary(),
         "ranks": {"f": rep["ranks_f"], "g": rep["ranks_g"], "out": rep["ranks_out"]},
+        "status_bits": rep["status_bits"],
     }
     if not a.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = oracle_run(cfg, eps, a.cpu_seconds)

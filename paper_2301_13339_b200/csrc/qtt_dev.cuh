@@ -514,13 +514,32 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, cplx* U_out, in
     Qd[NMAX - 1] = dgl[NMAX - 1];
 #pragma unroll
     for (int i = NMAX - 2; i >= 0; --i) Qd[i] = fma(dgl[i], Qd[i + 1], -e2[i] * Qd[i + 2]);
-    // twist r = argmax_{i < n} |P_i Q_{i+1}|
+    // twist: the j-th largest |P_i Q_{i+1}|, j = position of this eigenvalue
+    // inside a group of (near-)equal eigenvalues (gaps <= 1e-10 ||T||):
+    // members of a multiple eigenvalue of a numerically split T then localise
+    // in different blocks instead of repeating the same vector
+    int jc = 0;
+    for (int t2 = tid - 1; t2 >= 0; --t2) {
+      if (S.lam[n - 1 - t2] - S.lam[n - 2 - t2] > 1e-10) break;  // ranks t2, t2+1 not (near-)equal
+      ++jc;
+    }
     int r = 0;
-    double best = -1.0;
+    {
+      double prev = 1e308;
+      int prev_r = -1;
+      for (int rep = 0; rep <= jc; ++rep) {
+        double best = -1.0;
+        int rb = 0;
 #pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
-      const double v = (i < n) ? fabs(P[i] * Qd[i + 1]) : -2.0;
-      if (v > best) { best = v; r = i; }
+        for (int i = 0; i < NMAX; ++i) {
+          const double v = (i < n) ? fabs(P[i] * Qd[i + 1]) : -2.0;
+          const bool below = (v < prev) || (v == prev && i > prev_r);
+          if (below && v > best) { best = v; rb = i; }
+        }
+        prev = best;
+        prev_r = rb;
+        r = rb;
+      }
     }
     double z[NMAX];
     // i <= r: z_i = (-1)^{r-i} (prod_{k=i}^{r-1} e_k) P_i Q_{r+1}
