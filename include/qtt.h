@@ -97,13 +97,20 @@ typedef struct {
 
 /* Bytes of workspace needed by qtt_conv_full (and enough for any single
  * qtt_decompose / qtt_convolve / qtt_to_full of the same shape and caps).
- * Returns 0 for invalid arguments.  nranks: 1 (multi-GPU reserved). */
+ * Returns 0 for invalid arguments.  nranks = 1: single GPU (also enough for
+ * a 1-rank communicator); nranks = P > 1: per-rank bytes of the P-way
+ * column-sharded problem (one shard per rank, see "Multi-GPU" below). */
 size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec,
                            const qtt_trunc* fft, int nranks);
+/* Same, for the shards `comm` places in this process (comm may be NULL). */
+size_t qtt_comm_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec,
+                                const qtt_trunc* fft, qtt_comm_t comm);
 
 /* Step 1-2: max-rank TT-SVD (Alg. 1 + mod (1)) of the batch of
  * arrays x (shape->batch of them, stride shape->f_stride).  Writes a new
- * handle to *out whose device storage lives in ws. */
+ * handle to *out whose device storage lives in ws.  With comm != NULL, x is
+ * this process's shard(s) of the single (batch 1) global array and the
+ * handle holds the global cores, identical on every rank. */
 qtt_status qtt_decompose(const double* x, const qtt_shape* shape,
                          const qtt_trunc* dec, void* ws, size_t ws_bytes,
                          void* stream, qtt_comm_t comm, qtt_tt_t* out);
@@ -126,11 +133,13 @@ qtt_status qtt_convolve(qtt_tt_t f, qtt_tt_t g, const qtt_trunc* fft,
 
 /* Step 4 (Alg. 3): y = Re(full(t)) written in the caller layout
  * (batch stride y_stride of t's shape).  If y_imag != NULL the imaginary
- * part is written there too (diagnostics). */
+ * part is written there too (diagnostics).  With comm != NULL only this
+ * process's shard(s) of y are written (no communication). */
 qtt_status qtt_to_full(qtt_tt_t t, double* y, double* y_imag, void* ws,
                        size_t ws_bytes, void* stream, qtt_comm_t comm);
 
-/* Alg. 2 end to end: y = QTT convolution of f and g (Steps 1-4). */
+/* Alg. 2 end to end: y = QTT convolution of f and g (Steps 1-4).  With
+ * comm != NULL, f, g and y are this process's shards (batch 1). */
 qtt_status qtt_conv_full(const double* f, const double* g, double* y,
                          const qtt_shape* shape, const qtt_trunc* dec,
                          const qtt_trunc* fft, const long long shift[2],
@@ -146,6 +155,45 @@ qtt_status qtt_ranks(qtt_tt_t t, int index, int* ranks_host, int cap);
 int qtt_ndims(qtt_tt_t t);
 /* Releases the host handle (device storage belongs to the workspace). */
 void qtt_destroy(qtt_tt_t t);
+
+/* ------------------------------------------------------------ Multi-GPU
+ * Column sharding of the TT-SVD unfoldings (north star
+ * "the column dimension of each unfolding is sharded over GPUs, and the tiny
+ * Gram matrices are combined with an NCCL allreduce"):
+ *   - P = 2^l shards.  Shard s holds the QTT index range
+ *     [s 2^{d-l}, (s+1) 2^{d-l}), i.e. the elements whose top l QTT bits
+ *     equal s; it is stored as a dense row-major sub-image (1D: a contiguous
+ *     range; concat: a block of rows; interleaved: P=2 row halves, P=4
+ *     quadrants, ...), see qtt_shard_geometry.  d - l >= 12 is required.
+ *   - Alg. 1 steps k <= d - l: every column of the k-th unfolding lies in
+ *     one shard, so its Gram is the sum of the shards' Grams (one
+ *     ncclAllReduce of f's and g's Grams per step); the projection is local.
+ *     When a shard's unfolding gets narrower than 256 columns the small
+ *     remainder W is all-gathered and the last steps, the QTT-FFT chain and
+ *     the rounding run redundantly (bitwise identical) on every rank.
+ *   - Expansion: shard s = full(C_1, ..., C_{d-l} C_{d-l+1}[s_1] ...
+ *     C_d[s_l]) — no communication.
+ *   Results differ from the single-GPU path only by summation order. */
+
+/* Rank 0 creates the NCCL unique id and broadcasts it (e.g. with
+ * torch.distributed); every rank then calls qtt_comm_init with its rank, the
+ * CUDA device of the rank current.  NCCL is loaded at run time (the one
+ * already in the process, else libnccl.so.2): QTT_ENCCL if unavailable.
+ * nranks must be a power of two; rank r holds shard r. */
+qtt_status qtt_comm_unique_id(unsigned char id_host[128]);
+qtt_status qtt_comm_init(const unsigned char id_host[128], int nranks, int rank,
+                         qtt_comm_t* out);
+/* TEST-ONLY: a communicator under which THIS process holds all nshards
+ * shards on one GPU (shard j at element offset j 2^{d-l} of the f / g / y
+ * pointers); the cross-shard Gram sums run as a kernel.  Lets one GPU run
+ * the sharded algorithm without ranks that wait on each other. */
+qtt_status qtt_comm_init_virtual(int nshards, qtt_comm_t* out);
+void qtt_comm_destroy(qtt_comm_t comm);
+/* Host only: where shard `shard` of nshards sits in the global array
+ * (origin_host = {x0, y0}) and its size in bits (bits_host = {bx, by};
+ * 1D: {bits, 0}).  QTT_EINVAL for invalid shapes / shard counts. */
+qtt_status qtt_shard_geometry(const qtt_shape* shape, int nshards, int shard,
+                              long long origin_host[2], int bits_host[2]);
 
 /* TEST-ONLY: Hermitian eigendecomposition of the n x n (n <= 32) complex
  * matrix A (device, column-major interleaved re/im doubles) by the small

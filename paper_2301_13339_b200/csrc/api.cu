@@ -3,6 +3,8 @@
 // Every compute step runs in the kernels of ttsvd.cu, qfft.cu, hround.cu and
 // expand.cu; this file only marshals pointers.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: the library is dlopen'ed at qtt_comm_init
 
 #include <cstdarg>
 #include <cstdint>
@@ -25,6 +27,18 @@ void count_launches(int n) { g_launches += n; }
 
 #define QTT_XSTR(x) #x
 #define QTT_STR(x) QTT_XSTR(x)
+
+// Communicator of the column-sharded path.  NCCL: one shard
+// per rank (shard = rank).  Virtual: all nshards shards live in this process
+// on one GPU (test / single-GPU emulation of the sharded algorithm; the
+// cross-shard sums are done by a kernel instead of a collective).
+struct qtt_comm_s {
+  int kind;        // 0 = NCCL, 1 = virtual
+  int nranks, rank;
+  int nshards;     // P (total shards)
+  int nlocal;      // shards held by this process
+  ncclComm_t nc;
+};
 
 struct qtt_tt_s {
   qtt_shape shape;
@@ -201,6 +215,8 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
     p.layout = s->layout;
     p.bx = s->bits[0];
     p.d = d;
+    p.dl = d;
+    p.gsum = nullptr;
     p.Wa = sc.Wa; p.Wb = sc.Wb; p.part = sc.part; p.proj = sc.proj; p.tau2 = sc.tau2;
     p.cores = tt.cores + (size_t)i * d * SLOT;
     p.ranks = tt.ranks + (size_t)i * 64;
@@ -319,6 +335,299 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
   return r;
 }
 
+// ------------------------------------------------------------------ NCCL
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*errStr)(ncclResult_t) = nullptr;
+};
+
+// The NCCL already loaded in the process (PyTorch's) is preferred; else the
+// system one.  No link-time dependency: the library loads without NCCL.
+NcclApi& nccl_api() {
+  static NcclApi a;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+    if (!h) { a.err = "libnccl.so.2 not found"; return; }
+    bool ok = true;
+    auto sym = [&](const char* n) { void* p = dlsym(h, n); ok = ok && p; return p; };
+    a.getUniqueId = (decltype(a.getUniqueId))sym("ncclGetUniqueId");
+    a.commInitRank = (decltype(a.commInitRank))sym("ncclCommInitRank");
+    a.commDestroy = (decltype(a.commDestroy))sym("ncclCommDestroy");
+    a.allReduce = (decltype(a.allReduce))sym("ncclAllReduce");
+    a.allGather = (decltype(a.allGather))sym("ncclAllGather");
+    a.groupStart = (decltype(a.groupStart))sym("ncclGroupStart");
+    a.groupEnd = (decltype(a.groupEnd))sym("ncclGroupEnd");
+    a.errStr = (decltype(a.errStr))sym("ncclGetErrorString");
+    a.ok = ok;
+    if (!ok) a.err = "libnccl is missing a required symbol";
+  });
+  return a;
+}
+
+qtt_status nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return QTT_OK;
+  NcclApi& a = nccl_api();
+  return fail(QTT_ENCCL, "%s: %s", what, a.errStr ? a.errStr(r) : "NCCL error");
+}
+
+// -------------------------------------------------------- shard geometry
+// Shard s of P = 2^l holds the QTT index range [s 2^{d-l}, (s+1) 2^{d-l})
+// (its top l QTT bits equal s), stored as a dense row-major sub-image.
+struct ShardGeom {
+  int l, dl;
+  int lbits[2];        // bits of the shard along x, y
+  long long origin[2]; // position of the shard in the global array
+};
+
+int ilog2_exact(long long P) {
+  if (P < 1 || (P & (P - 1))) return -1;
+  int l = 0;
+  while ((1ll << l) < P) ++l;
+  return l;
+}
+
+qtt_status shard_geom(const qtt_shape* s, int P, int shard, ShardGeom* g) {
+  qtt_status r;
+  if ((r = check_shape(s))) return r;
+  const int l = ilog2_exact(P);
+  if (l < 0) return fail(QTT_EINVAL, "number of shards %d is not a power of two", P);
+  if (shard < 0 || shard >= P) return fail(QTT_EINVAL, "shard %d outside [0, %d)", shard, P);
+  const int d = shape_d(s), dl = d - l;
+  if (dl < SHARD_MIN_DL)
+    return fail(QTT_EINVAL, "a shard must hold >= 2^%d elements (d - log2 P = %d)", SHARD_MIN_DL, dl);
+  g->l = l;
+  g->dl = dl;
+  if (s->D == 1) {
+    g->lbits[0] = dl; g->lbits[1] = 0;
+    g->origin[0] = (long long)shard << dl; g->origin[1] = 0;
+  } else if (s->layout == QTT_LAYOUT_CONCAT) {
+    if (l > s->bits[1]) return fail(QTT_EINVAL, "concat layout: log2 P must be <= bits of y");
+    g->lbits[0] = s->bits[0]; g->lbits[1] = s->bits[1] - l;
+    g->origin[0] = 0; g->origin[1] = (long long)shard << g->lbits[1];
+  } else {
+    // QTT position q (1-based): odd -> x-bit (q+1)/2, even -> y-bit q/2
+    g->lbits[0] = (dl + 1) / 2; g->lbits[1] = dl / 2;
+    g->origin[0] = g->origin[1] = 0;
+    for (int j = 0; j < l; ++j) {
+      const int q = dl + 1 + j;
+      const long long b = (shard >> j) & 1;
+      if (q & 1) g->origin[0] |= b << ((q + 1) / 2 - 1);
+      else g->origin[1] |= b << (q / 2 - 1);
+    }
+  }
+  return QTT_OK;
+}
+
+// ------------------------------------------------- sharded TT-SVD plan
+struct ShardDec {
+  int ntens = 0, nlocal = 0, P = 1, first = 0, d = 0, dl = 0;
+  std::vector<DecProb> sh, tn;
+  DecProb* sh_dev = nullptr;
+  DecProb* tn_dev = nullptr;
+  double* gsum = nullptr;   // ntens x 1024, contiguous (one allreduce per level)
+  double* gath = nullptr;   // all-gather landing buffer
+};
+
+long long gather_cols_cap(int P) { return P == 1 ? FIN_COLS_HOST : (128ll * P > FIN_COLS_HOST ? 128ll * P : FIN_COLS_HOST); }
+
+// xs[t]: this process's first shard of tensor t (further local shards follow
+// at + j 2^{dl}); tts[t]: the tensor's core storage.
+void plan_sharded_dec(Carver& cv, const qtt_shape* s, const ShardGeom& g, int P, int nlocal, int first,
+                      int ntens, const double* const* xs, const TTAlloc* tts, ShardDec& D) {
+  D.ntens = ntens; D.nlocal = nlocal; D.P = P; D.first = first; D.d = shape_d(s); D.dl = g.dl;
+  D.sh.assign((size_t)ntens * nlocal, DecProb{});
+  D.tn.assign(ntens, DecProb{});
+  D.gsum = cv.take<double>((size_t)ntens * 1024);
+  const long long gcols = gather_cols_cap(P);
+  D.gath = cv.take<double>((size_t)ntens * P * RS_GATHER * gcols);
+  for (int t = 0; t < ntens; ++t) {
+    DecProb& T = D.tn[t];
+    T.x = nullptr;
+    T.layout = s->layout;
+    T.bx = s->bits[0];
+    T.d = D.d;
+    T.dl = D.d;
+    T.gsum = D.gsum ? D.gsum + (size_t)t * 1024 : nullptr;
+    T.Wa = cv.take<double>((size_t)RC * gcols);
+    T.Wb = cv.take<double>((size_t)RC * gcols);
+    T.part = cv.take<double>((size_t)NBLK_MAX * 1024);
+    T.proj = cv.take<double>(32 * 16);
+    T.tau2 = cv.take<double>(1);
+    T.cores = tts[t].cores;
+    T.ranks = tts[t].ranks;
+    for (int j = 0; j < nlocal; ++j) {
+      DecProb& X = D.sh[(size_t)t * nlocal + j];
+      X = T;
+      X.x = xs[t] ? xs[t] + ((size_t)j << g.dl) : nullptr;
+      X.bx = g.lbits[0];
+      X.dl = g.dl;
+      X.Wa = cv.take<double>((size_t)RC << (g.dl - 5));
+      X.Wb = cv.take<double>((size_t)RC << (g.dl - 6));
+      X.part = cv.take<double>((size_t)NBLK_MAX * 1024);
+    }
+  }
+  D.sh_dev = cv.take<DecProb>(D.sh.size());
+  D.tn_dev = cv.take<DecProb>(D.tn.size());
+}
+
+// Gram of the current level: per-CTA partials -> gsum (sum over the local
+// shards) -> sum over ranks (NCCL allreduce, f and g in one call).
+qtt_status reduce_grams(ShardDec& D, const qtt_comm_s* comm, int nblk, cudaStream_t st) {
+  qtt_status r;
+  if ((r = cuda_check(launch_gram_reduce(D.sh_dev, D.ntens, D.nlocal, nblk, st), "gram reduce"))) return r;
+  if (comm->kind == 0)
+    return nccl_check(nccl_api().allReduce(D.gsum, D.gsum, (size_t)D.ntens * 1024, ncclDouble, ncclSum, comm->nc, st),
+                      "ncclAllReduce(Gram)");
+  return QTT_OK;
+}
+
+// Alg. 1 over column shards: steps k <= d - l use the summed Grams; W is
+// gathered once the local unfolding is too narrow; the remaining steps run
+// redundantly on every rank on the (small) gathered W.
+qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, cudaStream_t st) {
+  qtt_status r;
+  if ((r = cuda_check(cudaMemcpyAsync(D.sh_dev, D.sh.data(), D.sh.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
+                      "copy descriptors")))
+    return r;
+  if ((r = cuda_check(cudaMemcpyAsync(D.tn_dev, D.tn.data(), D.tn.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
+                      "copy descriptors")))
+    return r;
+  const int d = D.d, dl = D.dl, nsh = (int)D.sh.size();
+  int nblk = dec_nblk_loc(dl);
+  if ((r = cuda_check(launch_level_gram(D.sh_dev, nsh, nblk, prm.status, st), "level gram"))) return r;
+  if ((r = reduce_grams(D, comm, nblk, st))) return r;
+  if ((r = cuda_check(launch_level_solve(D.tn_dev, D.ntens, 0, prm, st), "level solve"))) return r;
+  int k = 5;
+  nblk = proj_nblk(1 << (dl - k));
+  if ((r = cuda_check(launch_project(true, D.sh_dev, nsh, k, nblk, 1, st), "project"))) return r;
+  if ((r = reduce_grams(D, comm, nblk, st))) return r;
+  int src_is_a = 1;
+  ++k;
+  while ((1ll << (dl - k + 1)) >= 256 && (1ll << (d - k + 1)) > FIN_COLS_HOST) {
+    if ((r = cuda_check(launch_step_solve(D.tn_dev, D.ntens, k, 0, prm, st), "step solve"))) return r;
+    nblk = proj_nblk(1 << (dl - k));
+    if ((r = cuda_check(launch_project(false, D.sh_dev, nsh, k, nblk, src_is_a, st), "project"))) return r;
+    if ((r = reduce_grams(D, comm, nblk, st))) return r;
+    src_is_a ^= 1;
+    ++k;
+  }
+  // gather W_{k-1}: r_{k-1} x nl per shard -> r_{k-1} x nl P on every rank
+  const long long nl = 1ll << (dl - k + 1);
+  if (comm->kind == 0) {
+    NcclApi& A = nccl_api();
+    if ((r = nccl_check(A.groupStart(), "ncclGroupStart"))) return r;
+    for (int t = 0; t < D.ntens; ++t) {
+      const double* src = src_is_a ? D.sh[t].Wa : D.sh[t].Wb;
+      double* dst = D.gath + (size_t)t * D.P * RS_GATHER * nl;
+      if ((r = nccl_check(A.allGather(src, dst, (size_t)RS_GATHER * nl, ncclDouble, comm->nc, st), "ncclAllGather(W)"))) {
+        A.groupEnd();
+        return r;
+      }
+    }
+    if ((r = nccl_check(A.groupEnd(), "ncclGroupEnd"))) return r;
+    if ((r = cuda_check(launch_gather_w(D.sh_dev, D.tn_dev, D.ntens, D.nlocal, k - 1, nl, src_is_a, D.gath, D.P, st),
+                        "gather")))
+      return r;
+  } else {
+    if ((r = cuda_check(launch_gather_w(D.sh_dev, D.tn_dev, D.ntens, D.nlocal, k - 1, nl, src_is_a, nullptr, D.P, st),
+                        "gather")))
+      return r;
+  }
+  // remaining steps on the gathered W (tn.Wa), identical on every rank
+  src_is_a = 1;
+  int prev_nb = 0;   // the Gram of step k is the reduced one in gsum
+  while ((1ll << (d - k + 1)) > FIN_COLS_HOST) {
+    if ((r = cuda_check(launch_step_solve(D.tn_dev, D.ntens, k, prev_nb, prm, st), "step solve"))) return r;
+    const int nb2 = proj_nblk(1 << (d - k));
+    if ((r = cuda_check(launch_project(false, D.tn_dev, D.ntens, k, nb2, src_is_a, st), "project"))) return r;
+    src_is_a ^= 1;
+    prev_nb = nb2;
+    ++k;
+  }
+  return cuda_check(launch_finish(D.tn_dev, D.ntens, k, src_is_a, prm, st), "finish");
+}
+
+// ----------------------------------------------- sharded expansion plan
+struct ShardEx {
+  std::vector<FoldProb> fp;
+  std::vector<ExProb> ex;
+  FoldProb* fp_dev = nullptr;
+  ExProb* ex_dev = nullptr;
+};
+
+void plan_sharded_expand(Carver& cv, const cplx* cores, const int* ranks, const ShardGeom& g, int nlocal, int first,
+                         double* y, ShardEx& E) {
+  E.fp.assign(nlocal, FoldProb{});
+  E.ex.assign(nlocal, ExProb{});
+  for (int j = 0; j < nlocal; ++j) {
+    FoldProb& f = E.fp[j];
+    f.cores = cores;
+    f.ranks = ranks;
+    f.out_cores = cv.take<cplx>((size_t)g.dl * SLOT);
+    f.out_ranks = cv.take<int>(64);
+    f.shard = first + j;
+    ExProb& e = E.ex[j];
+    e.cores = f.out_cores;
+    e.ranks = f.out_ranks;
+    e.y = y ? y + ((size_t)j << g.dl) : nullptr;
+    e.lsplit = cv.take<double>(256 * 32);
+  }
+  E.fp_dev = cv.take<FoldProb>(nlocal);
+  E.ex_dev = cv.take<ExProb>(nlocal);
+}
+
+qtt_status run_sharded_expand(ShardEx& E, const qtt_shape* s, const ShardGeom& g, int d, int imag, cudaStream_t st) {
+  qtt_status r;
+  const int n = (int)E.fp.size();
+  if ((r = cuda_check(cudaMemcpyAsync(E.fp_dev, E.fp.data(), n * sizeof(FoldProb), cudaMemcpyHostToDevice, st),
+                      "copy descriptors")))
+    return r;
+  if ((r = cuda_check(cudaMemcpyAsync(E.ex_dev, E.ex.data(), n * sizeof(ExProb), cudaMemcpyHostToDevice, st),
+                      "copy descriptors")))
+    return r;
+  if ((r = cuda_check(launch_fold_tail(E.fp_dev, n, d, g.l, st), "fold tail"))) return r;
+  ExParams P{g.dl, s->layout, g.lbits[0], imag};
+  return cuda_check(launch_expand(E.ex_dev, n, P, st), "expand launch");
+}
+
+qtt_status check_comm(const qtt_comm_s* c, const qtt_shape* s, ShardGeom* g) {
+  if (s->batch != 1) return fail(QTT_EINVAL, "sharded problems need batch == 1");
+  return shard_geom(s, c->nshards, 0, g);
+}
+
+int comm_first(const qtt_comm_s* c) { return c->kind == 0 ? c->rank : 0; }
+
+// Workspace of qtt_conv_full when sharded P ways with nlocal shards here.
+size_t ws_sharded(const qtt_shape* shape, const qtt_trunc* fft, int P, int nlocal) {
+  ShardGeom g;
+  if (shape->batch != 1 || shard_geom(shape, P, 0, &g)) return 0;
+  const int d = shape_d(shape);
+  Carver cv(nullptr);
+  cv.take<int>(64);
+  TTAlloc tt[2] = {take_tt(cv, 1, d), take_tt(cv, 1, d)};
+  TTAlloc Y = take_tt(cv, 1, d);
+  const double* xs[2] = {nullptr, nullptr};
+  ShardDec D;
+  plan_sharded_dec(cv, shape, g, P, nlocal, 0, 2, xs, tt, D);
+  run_convolve(tt[0].cores, tt[0].ranks, 1, tt[1].cores, tt[1].ranks, 1, shape, fft, nullptr, 1.0, Y, cv, nullptr,
+               nullptr);
+  ShardEx E;
+  plan_sharded_expand(cv, Y.cores, Y.ranks, g, nlocal, 0, nullptr, E);
+  return cv.off + 4096;
+}
+
 qtt_status check_ws(const Carver& cv, void* ws, size_t ws_bytes) {
   if (!ws) return fail(QTT_EINVAL, "workspace is NULL");
   if (((uintptr_t)ws & 255) != 0) return fail(QTT_EINVAL, "workspace must be 256-byte aligned");
@@ -352,8 +661,9 @@ const char* qtt_build_info(void) {
 }
 
 size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const qtt_trunc* fft, int nranks) {
-  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec") || check_trunc(fft, RH_MAX, "fft") || nranks != 1)
+  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec") || check_trunc(fft, RH_MAX, "fft") || nranks < 1)
     return 0;
+  if (nranks > 1) return ws_sharded(shape, fft, nranks, 1);
   const int d = shape_d(shape);
   const int nf = shape->batch, ng = shape->g_stride == 0 ? 1 : shape->batch;
   Carver cv(nullptr);
@@ -365,19 +675,49 @@ size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const q
   cv.take<DecProb>(nf + ng);
   run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, nullptr, 1.0, Y, cv, nullptr, nullptr);
   run_expand(Y.cores, Y.ranks, nf, d, nullptr, 0, shape, 0, cv, nullptr);
-  return cv.off + 4096;
+  const size_t one = ws_sharded(shape, fft, 1, 1);   // a 1-rank communicator takes the sharded path
+  return cv.off + 4096 > one ? cv.off + 4096 : one;
+}
+
+size_t qtt_comm_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const qtt_trunc* fft,
+                                qtt_comm_t comm) {
+  if (!comm) return qtt_workspace_bytes(shape, dec, fft, 1);
+  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec") || check_trunc(fft, RH_MAX, "fft")) return 0;
+  return ws_sharded(shape, fft, comm->nshards, comm->nlocal);
 }
 
 qtt_status qtt_decompose(const double* x, const qtt_shape* shape, const qtt_trunc* dec, void* ws,
                          size_t ws_bytes, void* stream, qtt_comm_t comm, qtt_tt_t* out) {
   qtt_status r;
   if ((r = check_shape(shape))) return r;
-  if ((r = check_trunc(dec, RC, "dec"))) return r;
   if (!x || !out) return fail(QTT_EINVAL, "x / out is NULL");
-  if (comm) return fail(QTT_EINVAL, "multi-GPU communicators are not supported by this build");
+  if ((r = check_trunc(dec, comm ? RS_GATHER : RC, "dec"))) return r;
   cudaError_t ce;
   if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
   const int d = shape_d(shape);
+  if (comm) {
+    ShardGeom g;
+    if ((r = check_comm(comm, shape, &g))) return r;
+    cudaStream_t st = (cudaStream_t)stream;
+    auto plan = [&](Carver& cv, int*& status, TTAlloc& tt, ShardDec& D) {
+      status = cv.take<int>(64);
+      tt = take_tt(cv, 1, d);
+      plan_sharded_dec(cv, shape, g, comm->nshards, comm->nlocal, comm_first(comm), 1, &x, &tt, D);
+    };
+    Carver dry(nullptr);
+    int* status;
+    TTAlloc tt;
+    ShardDec D;
+    plan(dry, status, tt, D);
+    if ((r = check_ws(dry, ws, ws_bytes))) return r;
+    Carver cv(ws);
+    plan(cv, status, tt, D);
+    if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
+    DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status};
+    if ((r = run_sharded_dec(D, comm, prm, st))) return r;
+    *out = new_handle(shape, 1, dec->rmax, tt, status, st);
+    return *out ? QTT_OK : fail(QTT_ENOMEM, "host allocation failed");
+  }
   const int n = shape->batch;
   const long long stride = shape->f_stride ? shape->f_stride : (1ll << d);
   cudaStream_t st = (cudaStream_t)stream;
@@ -461,10 +801,25 @@ qtt_status qtt_to_full(qtt_tt_t t, double* y, double* y_imag, void* ws, size_t w
                        qtt_comm_t comm) {
   qtt_status r;
   if (!t || !y) return fail(QTT_EINVAL, "t / y is NULL");
-  if (comm) return fail(QTT_EINVAL, "multi-GPU communicators are not supported by this build");
   cudaError_t ce;
   if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
   const int d = t->d;
+  if (comm) {
+    ShardGeom g;
+    if ((r = check_comm(comm, &t->shape, &g))) return r;
+    if (t->nt != 1) return fail(QTT_EINVAL, "sharded expansion needs a single tensor");
+    cudaStream_t st = (cudaStream_t)stream;
+    Carver dry(nullptr);
+    ShardEx E;
+    plan_sharded_expand(dry, t->cores, t->ranks, g, comm->nlocal, comm_first(comm), y, E);
+    if ((r = check_ws(dry, ws, ws_bytes))) return r;
+    for (int im = 0; im < (y_imag ? 2 : 1); ++im) {
+      Carver cv(ws);
+      plan_sharded_expand(cv, t->cores, t->ranks, g, comm->nlocal, comm_first(comm), im ? y_imag : y, E);
+      if ((r = run_sharded_expand(E, &t->shape, g, d, im, st))) return r;
+    }
+    return QTT_OK;
+  }
   const long long ys = t->shape.y_stride ? t->shape.y_stride : (1ll << d);
   cudaStream_t st = (cudaStream_t)stream;
   Carver dry(nullptr);
@@ -487,8 +842,10 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   if ((r = check_trunc(dec, RS_XF, "dec"))) return r;
   if ((r = check_trunc(fft, RH_MAX, "fft"))) return r;
   if (!f || !g || !y) return fail(QTT_EINVAL, "f / g / y is NULL");
-  if (comm) return fail(QTT_EINVAL, "multi-GPU communicators are not supported by this build");
-  const size_t need = qtt_workspace_bytes(shape, dec, fft, 1);
+  ShardGeom geo{};
+  if (comm && (r = check_comm(comm, shape, &geo))) return r;
+  const size_t need = comm ? ws_sharded(shape, fft, comm->nshards, comm->nlocal)
+                           : qtt_workspace_bytes(shape, dec, fft, 1);
   if (!ws) return fail(QTT_EINVAL, "workspace is NULL");
   if (((uintptr_t)ws & 255) != 0) return fail(QTT_EINVAL, "workspace must be 256-byte aligned");
   if (ws_bytes < need) return fail(QTT_ENOMEM, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
@@ -511,8 +868,16 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   TTAlloc F = take_tt(cv, nf, d), G = take_tt(cv, ng, d), Y = take_tt(cv, nf, d);
   if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
   prof_mark(0, st);
-  // Step 1-2: all signals and the kernel(s) in one batched TT-SVD
-  {
+  DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status};
+  if (comm) {
+    // Step 1-2 column-sharded: f and g shards in one sequence, one allreduce per level
+    const double* xs[2] = {f, g};
+    TTAlloc tts[2] = {F, G};
+    ShardDec D;
+    plan_sharded_dec(cv, shape, geo, comm->nshards, comm->nlocal, comm_first(comm), 2, xs, tts, D);
+    if ((r = run_sharded_dec(D, comm, prm, st))) return r;
+  } else {
+    // Step 1-2: all signals and the kernel(s) in one batched TT-SVD
     const int d_ = d;
     std::vector<DecProb> h(nf + ng);
     for (int i = 0; i < nf + ng; ++i) {
@@ -524,6 +889,8 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
       p.layout = shape->layout;
       p.bx = shape->bits[0];
       p.d = d_;
+      p.dl = d_;
+      p.gsum = nullptr;
       p.Wa = sc.Wa; p.Wb = sc.Wb; p.part = sc.part; p.proj = sc.proj; p.tau2 = sc.tau2;
       p.cores = (isf ? F.cores : G.cores) + (size_t)j * d_ * SLOT;
       p.ranks = (isf ? F.ranks : G.ranks) + (size_t)j * 64;
@@ -532,7 +899,6 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
     if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), h.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
                         "copy descriptors")))
       return r;
-    DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status};
     if ((r = cuda_check(launch_ttsvd(dp, nf + ng, d_, prm, st), "TT-SVD launch"))) return r;
   }
   prof_mark(1, st);
@@ -540,7 +906,13 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   if ((r = run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, shift, scale, Y, cv, status, st)))
     return r;
   // Step 4
-  if ((r = run_expand(Y.cores, Y.ranks, nf, d, y, ys, shape, 0, cv, st))) return r;
+  if (comm) {
+    ShardEx E;
+    plan_sharded_expand(cv, Y.cores, Y.ranks, geo, comm->nlocal, comm_first(comm), y, E);
+    if ((r = run_sharded_expand(E, shape, geo, d, 0, st))) return r;
+  } else if ((r = run_expand(Y.cores, Y.ranks, nf, d, y, ys, shape, 0, cv, st))) {
+    return r;
+  }
   prof_mark(5, st);
   if (cv.off > ws_bytes) return fail(QTT_ENOMEM, "internal: workspace plan overflow");
   if (rep_host) {
@@ -630,5 +1002,66 @@ qtt_status qtt_debug_tt_from_host(const qtt_shape* shape, const void* cores_host
 }
 
 void qtt_destroy(qtt_tt_t t) { delete t; }
+
+qtt_status qtt_comm_unique_id(unsigned char id_host[128]) {
+  if (!id_host) return fail(QTT_EINVAL, "id is NULL");
+  NcclApi& A = nccl_api();
+  if (!A.ok) return fail(QTT_ENCCL, "NCCL unavailable: %s", A.err.c_str());
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  qtt_status r;
+  if ((r = nccl_check(A.getUniqueId(&id), "ncclGetUniqueId"))) return r;
+  memcpy(id_host, &id, 128);
+  return QTT_OK;
+}
+
+qtt_status qtt_comm_init(const unsigned char id_host[128], int nranks, int rank, qtt_comm_t* out) {
+  if (!id_host || !out) return fail(QTT_EINVAL, "id / out is NULL");
+  if (nranks < 1 || ilog2_exact(nranks) < 0) return fail(QTT_EINVAL, "nranks = %d is not a power of two", nranks);
+  if (rank < 0 || rank >= nranks) return fail(QTT_EINVAL, "rank %d outside [0, %d)", rank, nranks);
+  NcclApi& A = nccl_api();
+  if (!A.ok) return fail(QTT_ENCCL, "NCCL unavailable: %s", A.err.c_str());
+  ncclUniqueId id;
+  memcpy(&id, id_host, 128);
+  ncclComm_t nc;
+  qtt_status r;
+  if ((r = nccl_check(A.commInitRank(&nc, nranks, id, rank), "ncclCommInitRank"))) return r;
+  qtt_comm_t c = new (std::nothrow) qtt_comm_s{0, nranks, rank, nranks, 1, nc};
+  if (!c) {
+    A.commDestroy(nc);
+    return fail(QTT_ENOMEM, "host allocation failed");
+  }
+  *out = c;
+  return QTT_OK;
+}
+
+qtt_status qtt_comm_init_virtual(int nshards, qtt_comm_t* out) {
+  if (!out) return fail(QTT_EINVAL, "out is NULL");
+  if (nshards < 1 || ilog2_exact(nshards) < 0)
+    return fail(QTT_EINVAL, "nshards = %d is not a power of two", nshards);
+  qtt_comm_t c = new (std::nothrow) qtt_comm_s{1, 1, 0, nshards, nshards, nullptr};
+  if (!c) return fail(QTT_ENOMEM, "host allocation failed");
+  *out = c;
+  return QTT_OK;
+}
+
+void qtt_comm_destroy(qtt_comm_t c) {
+  if (!c) return;
+  if (c->kind == 0 && c->nc) nccl_api().commDestroy(c->nc);
+  delete c;
+}
+
+qtt_status qtt_shard_geometry(const qtt_shape* shape, int nshards, int shard, long long origin_host[2],
+                              int bits_host[2]) {
+  if (!origin_host || !bits_host) return fail(QTT_EINVAL, "origin / bits is NULL");
+  ShardGeom g;
+  qtt_status r;
+  if ((r = shard_geom(shape, nshards, shard, &g))) return r;
+  origin_host[0] = g.origin[0];
+  origin_host[1] = g.origin[1];
+  bits_host[0] = g.lbits[0];
+  bits_host[1] = g.lbits[1];
+  return QTT_OK;
+}
 
 }  // extern "C"

@@ -220,6 +220,54 @@ __global__ void __launch_bounds__(NT, 2) k_expand_main(const ExProb* probs, ExPa
   }
 }
 
+// ------------------------------------------------------- shard tail fold
+// One CTA per shard: v = C_{d-l+1}[b_1] ... C_d[b_l] (b = bits of `shard`,
+// LSB at position d-l+1), then out = (C_1 .. C_{d-l-1}, C_{d-l} v).
+__global__ void k_fold_tail(const FoldProb* probs, int d, int l) {
+  const FoldProb& pr = probs[blockIdx.x];
+  __shared__ cplx v[2][RC];
+  const int tid = threadIdx.x, dl = d - l;
+  if (tid < RC) v[0][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  int cur = 0;
+  for (int k = d; k > dl; --k) {
+    const int r0 = pr.ranks[k - 1], r1 = pr.ranks[k];
+    const int be = (pr.shard >> (k - dl - 1)) & 1;
+    const cplx* c = pr.cores + (size_t)(k - 1) * SLOT;
+    if (tid < r0) {
+      cplx s = czero();
+      for (int j = 0; j < r1; ++j) s = cfma(c[tid + r0 * be + 2 * r0 * j], v[cur][j], s);
+      v[cur ^ 1][tid] = s;
+    }
+    __syncthreads();
+    cur ^= 1;
+  }
+  // core dl folded with v: (r0, 2, r1) -> (r0, 2, 1)
+  {
+    const int r0 = pr.ranks[dl - 1], r1 = pr.ranks[dl];
+    const cplx* c = pr.cores + (size_t)(dl - 1) * SLOT;
+    cplx* o = pr.out_cores + (size_t)(dl - 1) * SLOT;
+    for (int e = tid; e < 2 * r0; e += blockDim.x) {
+      cplx s = czero();
+      for (int j = 0; j < r1; ++j) s = cfma(c[e + 2 * r0 * j], v[cur][j], s);
+      o[e] = s;
+    }
+  }
+  for (int k = 1; k < dl; ++k) {
+    const int n = 2 * pr.ranks[k - 1] * pr.ranks[k];
+    const cplx* c = pr.cores + (size_t)(k - 1) * SLOT;
+    cplx* o = pr.out_cores + (size_t)(k - 1) * SLOT;
+    for (int e = tid; e < n; e += blockDim.x) o[e] = c[e];
+  }
+  for (int k = tid; k < 64; k += blockDim.x) pr.out_ranks[k] = k < dl ? pr.ranks[k] : (k == dl ? 1 : 0);
+}
+
+cudaError_t launch_fold_tail(const FoldProb* probs_dev, int nprob, int d, int l, cudaStream_t st) {
+  k_fold_tail<<<nprob, 256, 0, st>>>(probs_dev, d, l);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
 static constexpr size_t PREP_SMEM = 2 * 256 * RC * sizeof(cplx);
 
 cudaError_t setup_expand_kernels() {

@@ -25,8 +25,10 @@ static constexpr int RH_MAX = 8;          // Rhat cap supported by the Hadamard 
 
 // ---------------------------------------------------------------- TT-SVD
 struct DecProb {
-  const double* x;   // input array (caller layout)
-  int layout, bx, d;
+  const double* x;   // input array (caller layout; a shard's sub-array when sharded)
+  int layout, bx, d; // bx: bits of the row stride of x; d: global number of modes
+  int dl;            // QTT bits held in x (d - log2 P for a shard, else d)
+  double* gsum;      // reduced Gram (1024 doubles) when the Gram is combined across shards
   double* Wa;        // ping-pong unfolding buffers
   double* Wb;
   double* part;      // per-CTA partial Grams [NBLK_MAX][32*32]
@@ -43,6 +45,30 @@ struct DecParams {
 };
 cudaError_t setup_ttsvd_kernels();
 cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st);
+
+// Column-sharded TT-SVD: the steps, launched one by one by the
+// host driver in api.cu, which inserts the cross-rank collectives.  `sh`
+// holds ntens * nlocal shard descriptors (tensor-major), `tn` ntens tensor
+// descriptors; shards of a tensor share its cores / ranks / proj / tau2 /
+// gsum.  nblk == 0 in a solve step means "read the reduced Gram gsum".
+int dec_nblk_loc(int dl);                                   // CTAs of the level-1 Gram pass
+int proj_nblk(int ncols);                                   // CTAs of a projection pass
+static constexpr int FIN_COLS_HOST = 256;                   // finisher: W columns it holds
+cudaError_t launch_level_gram(const DecProb* sh, int nsh, int nblk, int* status, cudaStream_t st);
+cudaError_t launch_gram_reduce(const DecProb* sh, int ntens, int nlocal, int nblk, cudaStream_t st);
+cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st);
+cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st);
+cudaError_t launch_project(bool from_x, const DecProb* pr, int nprob, int k, int nblk, int src_is_a,
+                           cudaStream_t st);
+cudaError_t launch_finish(const DecProb* tn, int ntens, int k, int src_is_a, DecParams prm, cudaStream_t st);
+// W_{k} of every shard (r_k x nl local columns, in the shard's src buffer)
+// -> tn.Wa (r_k x nl*nshards, shard-major columns).  Local shards: read
+// directly (gathered = nullptr); after an all-gather: from `gathered`
+// (ntens blocks of nshards x RS_GATHER*nl doubles).
+static constexpr int RS_GATHER = 10;
+static constexpr int SHARD_MIN_DL = 12;   // a shard holds >= 2^12 elements (one Gram chunk)
+cudaError_t launch_gather_w(const DecProb* sh, const DecProb* tn, int ntens, int nlocal, int k, long long nl,
+                            int src_is_a, const double* gathered, int nshards, cudaStream_t st);
 
 // ------------------------------------------------------------- transforms
 struct XfProb {
@@ -106,5 +132,17 @@ struct ExParams {
 };
 cudaError_t setup_expand_kernels();
 cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& prm, cudaStream_t st);
+
+// Sharded expansion: the shard whose top l QTT bits equal
+// `shard` is full(C_1 .. C_{d-l-1}, C_{d-l} v) with v = C_{d-l+1}[b_1] ..
+// C_d[b_l]; k_fold_tail writes those d-l cores into out_cores/out_ranks.
+struct FoldProb {
+  const cplx* cores;
+  const int* ranks;
+  cplx* out_cores;   // (d - l) slots
+  int* out_ranks;    // 64 ints
+  int shard;
+};
+cudaError_t launch_fold_tail(const FoldProb* probs_dev, int nprob, int d, int l, cudaStream_t st);
 
 }  // namespace qtt

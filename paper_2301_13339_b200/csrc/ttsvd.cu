@@ -119,8 +119,7 @@ __global__ void __launch_bounds__(NT) k_level_gram(const DecProb* probs, int nbl
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ double smem[];
   double* buf[2] = {smem, smem + CHUNK_SMEM};
-  const int d = pr.d;
-  const uint64_t nchunks = 1ull << (d - 12);
+  const uint64_t nchunks = 1ull << (pr.dl - 12);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   double acc[10][2];
 #pragma unroll
@@ -190,6 +189,7 @@ __global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nb
   constexpr int LD = EigSmem<32>::LD;
   for (int e = tid; e < 1024; e += NT) {
     double s = 0.0;
+    if (nblk == 0) s = pr.gsum[e];   // Gram already reduced (across shards)
     for (int b = 0; b < nblk; ++b) s += pr.part[(size_t)b * 1024 + e];
     S.G[e] = s;
   }
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(NT) k_project(const DecProb* probs, int k, int
   if ((kp & 7) == 0) kp += 4;
   const double* src = FROM_X ? nullptr : (src_is_a ? pr.Wa : pr.Wb);
   double* dst = FROM_X ? pr.Wa : (src_is_a ? pr.Wb : pr.Wa);
-  const uint64_t ncols = 1ull << (d - k);        // columns of W_k
+  const uint64_t ncols = 1ull << (pr.dl - k);    // (local) columns of W_k
   const uint64_t nchunks = ncols / 128;
   // projector fragments: A = P^T (r x krows): a[mb][ks] = P[4ks + lane&3][8mb + lane>>2]
   double afr[2][8];
@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
   for (int e = tid; e < rr * rr; e += NT) {
     int i = e % rr, j = e / rr;
     double s = 0.0;
+    if (nblk == 0) s = pr.gsum[i * 32 + j];   // Gram already reduced (across shards)
     for (int b = 0; b < nblk; ++b) s += pr.part[(size_t)b * 1024 + i * 32 + j];
     S.E.A[0][i + LD * j] = cmk(s, 0.0);
   }
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
 // ------------------------------------------------------------------- K4
 static constexpr int FIN_CAP = 4096;             // doubles of W_{k-1} the finisher holds
 static constexpr int FIN_COLS = FIN_CAP / RC;     // 256 columns at the rank cap
+static_assert(FIN_COLS == FIN_COLS_HOST, "host driver mirrors FIN_COLS");
 static constexpr int FIN_D = 12;                  // d <= 12: whole TT-SVD in one CTA
 struct FinishSmem {
   double B[2][FIN_CAP];
@@ -516,12 +518,112 @@ __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart,
   if (tid == 0) pr.ranks[d] = 1;
 }
 
-// ------------------------------------------------------------ host driver
 size_t smem_level_gram() { return 2 * CHUNK_SMEM * sizeof(double); }
 size_t smem_level_solve() { return sizeof(LevelSolveSmem); }
 size_t smem_project() { return sizeof(ProjSmem); }
 size_t smem_step_solve() { return sizeof(StepSolveSmem); }
 size_t smem_finish() { return sizeof(FinishSmem); }
+
+// ------------------------------------------------- sharded-path helpers
+// gsum_t = sum over the tensor's local shards j (in order) of sum over the
+// per-CTA partials b.  Grid (32, ntens): CTA x owns 32 Gram entries, its 8
+// warps split the partials and are combined in a fixed order.
+__global__ void __launch_bounds__(NT) k_gram_reduce(const DecProb* sh, int nlocal, int nblk) {
+  __shared__ double red[NT / 32][32];
+  const int t = blockIdx.y, lane = threadIdx.x & 31, wb = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  double tot = 0.0;
+  for (int j = 0; j < nlocal; ++j) {
+    const DecProb& pr = sh[t * nlocal + j];
+    double s = 0.0;
+    for (int b = wb; b < nblk; b += NT / 32) s += pr.part[(size_t)b * 1024 + e];
+    red[wb][lane] = s;
+    __syncthreads();
+    if (wb == 0) {
+      double u = 0.0;
+#pragma unroll
+      for (int q = 0; q < NT / 32; ++q) u += red[q][lane];
+      tot += u;
+    }
+    __syncthreads();
+  }
+  if (wb == 0) sh[t * nlocal].gsum[e] = tot;
+}
+
+// tn[t].Wa[:, nl j + c] = W_k of shard j, column c (r_k rows).  Source: the
+// local shards' ping-pong buffer, or the all-gathered blocks of RS_GATHER*nl.
+__global__ void __launch_bounds__(NT) k_gather_w(const DecProb* sh, const DecProb* tn, int nlocal, int k,
+                                                 long long nl, int src_is_a, const double* gathered,
+                                                 int nshards) {
+  const int t = blockIdx.y;
+  const DecProb& T = tn[t];
+  const int r = T.ranks[k];
+  const long long blk = (long long)r * nl;
+  for (int j = 0; j < nshards; ++j) {
+    const double* src;
+    if (gathered) src = gathered + ((size_t)t * nshards + j) * (size_t)(RS_GATHER * nl);
+    else src = src_is_a ? sh[t * nlocal + j].Wa : sh[t * nlocal + j].Wb;
+    for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < blk; e += (long long)gridDim.x * NT)
+      T.Wa[j * blk + e] = src[e];
+  }
+}
+
+int dec_nblk_loc(int dl) {
+  uint64_t nchunks = 1ull << (dl - 12);
+  return (int)(nchunks < (uint64_t)NBLK_MAX ? nchunks : (uint64_t)NBLK_MAX);
+}
+
+int proj_nblk(int ncols) {
+  int nc = ncols / 128;
+  return nc < NBLK_MAX ? nc : NBLK_MAX;
+}
+
+cudaError_t launch_level_gram(const DecProb* sh, int nsh, int nblk, int* status, cudaStream_t st) {
+  k_level_gram<<<dim3(nblk, nsh), NT, smem_level_gram(), st>>>(sh, nblk, status);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_reduce(const DecProb* sh, int ntens, int nlocal, int nblk, cudaStream_t st) {
+  k_gram_reduce<<<dim3(32, ntens), NT, 0, st>>>(sh, nlocal, nblk);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st) {
+  k_level_solve<<<dim3(1, ntens), NT, smem_level_solve(), st>>>(tn, nblk, prm);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st) {
+  k_step_solve<<<dim3(1, ntens), NT, smem_step_solve(), st>>>(tn, k, nblk, prm);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_project(bool from_x, const DecProb* pr, int nprob, int k, int nblk, int src_is_a,
+                           cudaStream_t st) {
+  if (from_x) k_project<true><<<dim3(nblk, nprob), NT, smem_project(), st>>>(pr, k, nblk, src_is_a);
+  else k_project<false><<<dim3(nblk, nprob), NT, smem_project(), st>>>(pr, k, nblk, src_is_a);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finish(const DecProb* tn, int ntens, int k, int src_is_a, DecParams prm, cudaStream_t st) {
+  k_finish<<<dim3(1, ntens), NT, smem_finish(), st>>>(tn, k, src_is_a, prm);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_w(const DecProb* sh, const DecProb* tn, int ntens, int nlocal, int k, long long nl,
+                            int src_is_a, const double* gathered, int nshards, cudaStream_t st) {
+  k_gather_w<<<dim3(8, ntens), NT, 0, st>>>(sh, tn, nlocal, k, nl, src_is_a, gathered, nshards);
+  count_launches(1);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ host driver
 
 int dec_nblk(int d) {
   if (d <= FIN_D) return 0;

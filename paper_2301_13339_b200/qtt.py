@@ -21,7 +21,8 @@ SYMBOLS = [
     "qtt_to_full", "qtt_conv_full", "qtt_wait", "qtt_ranks", "qtt_ndims",
     "qtt_destroy", "qtt_status_string", "qtt_last_error", "qtt_build_info",
     "qtt_debug_eigh", "qtt_debug_tt_from_host", "qtt_profile_enable", "qtt_profile_read",
-    "qtt_launch_count",
+    "qtt_launch_count", "qtt_comm_workspace_bytes", "qtt_comm_unique_id", "qtt_comm_init",
+    "qtt_comm_init_virtual", "qtt_comm_destroy", "qtt_shard_geometry",
 ]
 
 
@@ -96,6 +97,18 @@ def lib():
     L.qtt_profile_read.argtypes = [ctypes.POINTER(ctypes.c_float), I]
     L.qtt_launch_count.restype = ctypes.c_longlong
     L.qtt_launch_count.argtypes = []
+    L.qtt_comm_workspace_bytes.restype = S
+    L.qtt_comm_workspace_bytes.argtypes = [pS, pT, pT, P]
+    L.qtt_comm_unique_id.restype = I
+    L.qtt_comm_unique_id.argtypes = [ctypes.c_char_p]
+    L.qtt_comm_init.restype = I
+    L.qtt_comm_init.argtypes = [ctypes.c_char_p, I, I, pH]
+    L.qtt_comm_init_virtual.restype = I
+    L.qtt_comm_init_virtual.argtypes = [I, pH]
+    L.qtt_comm_destroy.restype = None
+    L.qtt_comm_destroy.argtypes = [P]
+    L.qtt_shard_geometry.restype = I
+    L.qtt_shard_geometry.argtypes = [pS, I, I, pLL, ctypes.POINTER(ctypes.c_int)]
     L.qtt_debug_tt_from_host.restype = I
     L.qtt_debug_tt_from_host.argtypes = [pS, P, ctypes.POINTER(ctypes.c_int), I, P, S, P, pH]
     _LIB = L
@@ -153,10 +166,10 @@ def qtt_workspace_bytes(shp, dec, fft, nranks=1):
     return n
 
 
-def qtt_decompose(x_ptr, shp, dec, ws_ptr, ws_bytes, stream=0, ws_owner=None):
+def qtt_decompose(x_ptr, shp, dec, ws_ptr, ws_bytes, stream=0, ws_owner=None, comm=None):
     h = ctypes.c_void_p()
     _check(lib().qtt_decompose(x_ptr, ctypes.byref(shp), ctypes.byref(dec), ws_ptr, ws_bytes,
-                               stream, None, ctypes.byref(h)))
+                               stream, _comm(comm), ctypes.byref(h)))
     return TT(h, ws_owner)
 
 
@@ -174,22 +187,79 @@ def qtt_convolve(f, g, fft, shift, scale, ws_ptr, ws_bytes, stream=0, ws_owner=N
     return TT(h, ws_owner)
 
 
-def qtt_to_full(tt, y_ptr, ws_ptr, ws_bytes, stream=0, y_imag_ptr=None):
-    _check(lib().qtt_to_full(tt.h, y_ptr, y_imag_ptr, ws_ptr, ws_bytes, stream, None))
+def qtt_to_full(tt, y_ptr, ws_ptr, ws_bytes, stream=0, y_imag_ptr=None, comm=None):
+    _check(lib().qtt_to_full(tt.h, y_ptr, y_imag_ptr, ws_ptr, ws_bytes, stream, _comm(comm)))
 
 
 def qtt_conv_full(f_ptr, g_ptr, y_ptr, shp, dec, fft, shift, scale, ws_ptr, ws_bytes, stream=0,
-                  report=False):
+                  report=False, comm=None):
     rep = Report() if report else None
     _check(lib().qtt_conv_full(f_ptr, g_ptr, y_ptr, ctypes.byref(shp), ctypes.byref(dec),
                                ctypes.byref(fft), _shift(shift), float(scale), ws_ptr, ws_bytes,
-                               stream, None, ctypes.byref(rep) if rep is not None else None))
+                               stream, _comm(comm), ctypes.byref(rep) if rep is not None else None))
     if rep is None:
         return None
     d = rep.d
     return {"d": d, "ranks_f": list(rep.ranks_f[:d + 1]), "ranks_g": list(rep.ranks_g[:d + 1]),
             "ranks_out": list(rep.ranks_out[:d + 1]), "ms_total": rep.ms_total,
             "status_bits": rep.status_bits}
+
+
+class Comm:
+    """Owning wrapper of a qtt_comm_t (NCCL or virtual shards)."""
+
+    def __init__(self, handle, nshards, nlocal, first):
+        self.h = handle
+        self.nshards = nshards      # P
+        self.nlocal = nlocal        # shards held by this process
+        self.first = first          # index of this process's first shard
+
+    def close(self):
+        if getattr(self, "h", None) and _LIB is not None:
+            _LIB.qtt_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def _comm(comm):
+    return None if comm is None else comm.h
+
+
+def qtt_comm_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().qtt_comm_unique_id(buf))
+    return buf.raw
+
+
+def qtt_comm_init(uid, nranks, rank):
+    """NCCL communicator; `uid` = rank 0's qtt_comm_unique_id() bytes."""
+    h = ctypes.c_void_p()
+    _check(lib().qtt_comm_init(bytes(uid), nranks, rank, ctypes.byref(h)))
+    return Comm(h, nranks, 1, rank)
+
+
+def qtt_comm_init_virtual(nshards):
+    h = ctypes.c_void_p()
+    _check(lib().qtt_comm_init_virtual(nshards, ctypes.byref(h)))
+    return Comm(h, nshards, nshards, 0)
+
+
+def qtt_comm_workspace_bytes(shp, dec, fft, comm):
+    n = lib().qtt_comm_workspace_bytes(ctypes.byref(shp), ctypes.byref(dec), ctypes.byref(fft),
+                                       _comm(comm))
+    if n == 0:
+        raise QttError(QTT_EINVAL, "invalid shape / truncation / sharding")
+    return n
+
+
+def qtt_shard_geometry(shp, nshards, shard):
+    """(origin (x0, y0), bits (bx, by)) of a shard in the global array."""
+    o = (ctypes.c_longlong * 2)()
+    b = (ctypes.c_int * 2)()
+    _check(lib().qtt_shard_geometry(ctypes.byref(shp), nshards, shard, o, b))
+    return (int(o[0]), int(o[1])), (int(b[0]), int(b[1]))
 
 
 def build_info():
