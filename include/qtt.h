@@ -198,7 +198,9 @@ qtt_status qtt_shard_geometry(const qtt_shape* shape, int nshards, int shard,
 /* TEST-ONLY: Hermitian eigendecomposition of the n x n (n <= 32) complex
  * matrix A (device, column-major interleaved re/im doubles) by the small
  * eigensolver every truncation of the path uses (mode 0: tridiagonal solver
- * with Jacobi fallback; mode 1: Jacobi only).  lam (device, n): eigenvalues in
+ * with Jacobi fallback, all n vectors; mode 1: Jacobi only; mode m >= 2: the
+ * production solver asked for the m-1 leading vectors only, as the
+ * truncations do).  lam (device, n): eigenvalues in
  * descending order; U (device, n x n complex): eigenvectors; sweeps (device,
  * >= 2 ints): Jacobi sweeps, fallbacks taken; reps: repeat count (timing).
  * Stream-ordered. */

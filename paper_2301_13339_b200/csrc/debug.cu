@@ -19,7 +19,8 @@ __global__ void __launch_bounds__(NT) k_debug_eigh(const cplx* A, int n, double*
   for (int r = 0; r < reps; ++r) {
     for (int e = threadIdx.x; e < n * n; e += NT) E.A[0][(e % n) + LD * (e / n)] = A[e];
     __syncthreads();
-    V = mode ? jacobi_eig<NMAX, NT>(E, n, nullptr) : eig_small<NMAX, NT>(E, n, n, nullptr);
+    if (mode == 1) V = jacobi_eig<NMAX, NT>(E, n, nullptr);
+    else V = eig_small<NMAX, NT>(E, n, mode >= 2 ? mode - 1 : n, nullptr);
   }
   for (int e = threadIdx.x; e < n * n; e += NT) U[e] = V[(e % n) + LD * (e / n)];
   for (int i = threadIdx.x; i < n; i += NT) lam[i] = E.lam[i];

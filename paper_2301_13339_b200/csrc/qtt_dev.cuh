@@ -10,6 +10,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace qtt {
 
@@ -161,6 +162,10 @@ struct TridSmem {
   static constexpr int LD = NMAX + 1;
   cplx hv[NMAX * LD];        // Householder vector of column k in column k (rows k+1..)
   cplx w[NMAX];
+  cplx sub[NMAX];            // subdiagonal alpha_k of the reduced matrix
+  cplx colx[32];             // next reflector column (rows below the diagonal)
+  cplx colc[32];             // the column after it
+  cplx ypart[4][32];         // per-warp partial A x
   cplx ph[NMAX];             // D = diag(ph)
   double tau[NMAX];
   double dg[NMAX];           // diag of T (normalised)
@@ -173,6 +178,7 @@ struct TridSmem {
   long long tstep[5];        // clock64 per tridiagonalisation sub-phase (diagnostics)
   double anrm;
   int bad;
+  int prog;                  // reflectors published by the tridiagonalising warp
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -205,6 +211,37 @@ __device__ __forceinline__ double rcp_f64(double x) {
   return fma(y, e, y);
 }
 
+// ---- fast reciprocal / rsqrt: one MUFU op (fp32 approx) or MUFU + Newton
+// steps to full fp64 precision (no IEEE slow-path subroutine calls)
+__device__ __forceinline__ float frsqrt_fast(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float frcp_fast(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double drcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double drsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
 // number of eigenvalues of T below x: sign changes of p_0 = 1,
 // p_i = (dg_i - x) p_{i-1} - e2_{i-1} p_{i-2} (zero on the negative side)
 // T is padded to NMAX with decoupled diagonal entries 4.0 (above the spectrum
@@ -234,99 +271,8 @@ __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const doubl
   return cnt;
 }
 
-// Householder tridiagonalisation with the rows in registers (lane i holds row
-// i of the normalised A, n <= NMAX <= 32); all data exchange by shuffles.
-// Writes the reflectors (S.hv, S.tau), D (S.ph) and T (S.dg, S.of, S.e2).
-template <int NMAX>
-__device__ void trid_reduce_regs(TridSmem<NMAX>& S, const cplx* A0, int LDA, int n) {
-  constexpr int LD = NMAX + 1;
-  const int lane = threadIdx.x & 31;
-  cplx a[NMAX];
-#pragma unroll
-  for (int j = 0; j < NMAX; ++j) a[j] = (lane < n && j < n) ? A0[lane + LDA * j] : czero();
-#pragma unroll
-  for (int k = 0; k + 2 < NMAX; ++k) {
-    if (k + 2 < n) {
-      const bool act = lane > k && lane < n;
-      const cplx xi = act ? a[k] : czero();
-      const double s2 = warp_sum(cabs2(xi));
-      const cplx x0 = make_double2(__shfl_sync(0xffffffffu, xi.x, k + 1), __shfl_sync(0xffffffffu, xi.y, k + 1));
-      cplx vi = czero();
-      double tau = 0.0;
-      cplx alpha = czero();
-      if (s2 > 1e-60) {
-        const double rs = rsqrt_f64(s2);
-        const double sig = s2 * rs;
-        const double x02 = cabs2(x0);
-        cplx phs = cmk(1.0, 0.0);
-        double ax0 = 0.0;
-        if (x02 > 1e-60) {
-          const double r0 = rsqrt_f64(x02);
-          ax0 = x02 * r0;
-          phs = cscale(x0, r0);
-        }
-        alpha = cmk(-phs.x * sig, -phs.y * sig);
-        vi = (lane == k + 1) ? cscale(phs, ax0 + sig) : xi;
-        tau = rcp_f64(sig * (sig + ax0));
-      }
-      if (act) S.hv[lane + LD * k] = vi;
-      if (lane == 0) S.tau[k] = tau;
-      if (tau != 0.0) {
-        // p_i = tau sum_j a[j] v_j over j = k+1..n-1 (v_j broadcast)
-        cplx q0 = czero(), q1 = czero();
-#pragma unroll
-        for (int j = k + 1; j < NMAX; ++j) {
-          const cplx vj = make_double2(__shfl_sync(0xffffffffu, vi.x, j), __shfl_sync(0xffffffffu, vi.y, j));
-          if (j < n) {
-            if ((j - k) & 1) q0 = cfma(a[j], vj, q0);
-            else q1 = cfma(a[j], vj, q1);
-          }
-        }
-        const cplx p = act ? cscale(cadd(q0, q1), tau) : czero();
-        const double vp = warp_sum(vi.x * p.x + vi.y * p.y);
-        const double K = 0.5 * tau * vp;
-        const cplx wi = cmk(p.x - K * vi.x, p.y - K * vi.y);
-#pragma unroll
-        for (int j = k + 1; j < NMAX; ++j) {
-          const cplx wj = make_double2(__shfl_sync(0xffffffffu, wi.x, j), __shfl_sync(0xffffffffu, wi.y, j));
-          const cplx vj = make_double2(__shfl_sync(0xffffffffu, vi.x, j), __shfl_sync(0xffffffffu, vi.y, j));
-          if (act && j < n) a[j] = csub(a[j], cfma_bc(vi, wj, cmul(wi, cconj(vj))));
-        }
-      }
-      if (act) a[k] = (lane == k + 1) ? alpha : czero();
-    }
-  }
-  // T: diag dg_i = a[i] of lane i, subdiag beta_k = a[k] of lane k+1
-  double dgi = 0.0;
-#pragma unroll
-  for (int j = 0; j < NMAX; ++j) if (j == lane) dgi = a[j].x;
-  cplx bsub = czero();   // lane k+1 holds beta_k in a[k]
-#pragma unroll
-  for (int j = 0; j + 1 < NMAX; ++j) if (j + 1 == lane) bsub = a[j];
-  if (lane < n) S.dg[lane] = dgi;
-  if (lane >= 1 && lane < n) S.w[lane - 1] = bsub;
-  __syncwarp();
-  if (lane == 0) {
-    cplx ph = cmk(1.0, 0.0);
-    S.ph[0] = ph;
-    for (int k = 0; k + 1 < n; ++k) {
-      const cplx b = S.w[k];
-      const double ab2 = cabs2(b);
-      double ab = 0.0;
-      if (ab2 > 1e-60) {
-        const double r = rsqrt_f64(ab2);
-        ab = ab2 * r;
-        ph = cmul(ph, cscale(b, r));
-      }
-      S.ph[k + 1] = ph;
-      S.of[k] = ab;
-      S.e2[k] = ab * ab;
-    }
-  }
-}
-
 template <int NMAX, int NT>
-__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out) {
+__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x, lane = tid & 31;
   // ---- normalise by ||A||_F
@@ -339,104 +285,187 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     const int i = e % n, j = e / n;
     A0[i + LDA * j] = cscale(A0[i + LDA * j], inv);
   }
-  if (tid == 0) { S.bad = 0; S.anrm = anrm; }
+  if (tid == 0) { S.bad = 0; S.anrm = anrm; S.prog = 0; }
   __syncthreads();
   long long tt0 = clock64();
-  // ---- Householder tridiagonalisation.  Per step: warp 0 forms the
-  //      reflector; the whole CTA does the matvec p = tau B v (8 threads per
-  //      row, shuffle reduction) and the rank-2 update (one element each).
-  for (int k = 0; k + 2 < n; ++k) {
-    const int m = n - k - 1;
-    if (tid < 32) {
-      const int i = k + 1 + lane;
-      const cplx xi = (lane < m) ? A0[i + LDA * k] : czero();
-      const double s2 = warp_sum(cabs2(xi));
-      const cplx x0 = make_double2(__shfl_sync(0xffffffffu, xi.x, 0), __shfl_sync(0xffffffffu, xi.y, 0));
-      double tau = 0.0;
-      cplx vi = czero(), alpha = czero();
-      if (s2 > 1e-60) {
-        const double rs = rsqrt_f64(s2);
-        const double sig = s2 * rs;
-        const double x02 = cabs2(x0);
-        cplx phs = cmk(1.0, 0.0);
-        double ax0 = 0.0;
-        if (x02 > 1e-60) {
-          const double r0 = rsqrt_f64(x02);
-          ax0 = x02 * r0;
-          phs = cscale(x0, r0);
-        }
-        alpha = cmk(-phs.x * sig, -phs.y * sig);
-        vi = (lane == 0) ? cscale(phs, ax0 + sig) : xi;
-        tau = rcp_f64(sig * (sig + ax0));
-      }
-      if (lane < m) {
-        S.hv[i + LD * k] = vi;
-        A0[i + LDA * k] = (lane == 0) ? alpha : czero();
-      }
-      if (lane == 0) S.tau[k] = tau;
-    }
-    __syncthreads();
-    const double tau = S.tau[k];
-    if (tau != 0.0) {
-      // p_r = tau sum_j B[r][j] v_j, rows r < m: 8 threads per row
-      {
-        const int r = tid >> 3, part = tid & 7;
-        cplx q = czero();
-        if (r < m) {
+  // ---- Householder tridiagonalisation by warp 0 alone (lane = row, no CTA
+  //      barriers); warp 1 accumulates Q = H_0 H_1 ... H_{n-3} explicitly in
+  //      Qm as the reflectors appear (S.prog), so the back-transformation is
+  //      a plain product.
+  const int wp = tid >> 5;
+#ifdef QTT_TRID_TIMING
+  long long ts[4] = {0, 0, 0, 0}, tq = 0;
+#define TS_MARK(q) { long long _t = clock64(); ts[q] += _t - tq; tq = _t; }
+#else
+#define TS_MARK(q)
+#endif
+  static_assert(NT >= 160, "trid_values needs warps 0-3 (reduction) and 4 (Q)");
+  if (wp < 4) {
+    // Warps 0-3 (one per SM sub-partition, so the FP64 pipes of all four
+    // are used): lane i = row i, warp w owns columns j = w + 4t of the
+    // zero-padded matrix in registers.  Per step k ONE reduction, done
+    // redundantly by each warp: with x = column k below the diagonal,
+    // y = A x, c = A e_{k+1}: v = x + beta e_{k+1}, p = tau (y + beta c),
+    // v^H A v = x^H A x + beta x^H c + conj(beta) y_{k+1} + |beta|^2 c_{k+1}.
+    // Cross-warp traffic: partial y (smem) and the two next columns.
+    constexpr int TC = (NMAX + 3) / 4;
+    const int i = lane;
+    const bool live = i < NMAX;
+    const int ri = live ? i : 0;
+    cplx a[TC];
 #pragma unroll
-          for (int u = 0; u < (NMAX + 7) / 8; ++u) {
-            const int j = part + 8 * u;
-            if (j < m) q = cfma(A0[(k + 1 + r) + LDA * (k + 1 + j)], S.hv[k + 1 + j + LD * k], q);
-          }
-        }
-        q.x += __shfl_xor_sync(0xffffffffu, q.x, 1);
-        q.y += __shfl_xor_sync(0xffffffffu, q.y, 1);
-        q.x += __shfl_xor_sync(0xffffffffu, q.x, 2);
-        q.y += __shfl_xor_sync(0xffffffffu, q.y, 2);
-        q.x += __shfl_xor_sync(0xffffffffu, q.x, 4);
-        q.y += __shfl_xor_sync(0xffffffffu, q.y, 4);
-        if (r < m && part == 0) S.w[r] = cscale(q, tau);
-      }
-      __syncthreads();
-      // K = (tau/2) Re(v^H p); w = p - K v (warp 0)
-      if (tid < 32) {
-        const cplx pi = (lane < m) ? S.w[lane] : czero();
-        const cplx vi = (lane < m) ? S.hv[k + 1 + lane + LD * k] : czero();
-        const double vp = warp_sum(vi.x * pi.x + vi.y * pi.y);
-        const double K = 0.5 * tau * vp;
-        if (lane < m) S.w[lane] = cmk(pi.x - K * vi.x, pi.y - K * vi.y);
-      }
-      __syncthreads();
-      // B -= v w^H + w v^H, one element per thread
-      for (int e = tid; e < m * m; e += NT) {
-        const int r = e % m, c = e / m;
-        const cplx vr = S.hv[k + 1 + r + LD * k], vc = S.hv[k + 1 + c + LD * k];
-        const cplx wr = S.w[r], wc = S.w[c];
-        cplx* b = &A0[(k + 1 + r) + LDA * (k + 1 + c)];
-        *b = csub(*b, cfma_bc(vr, wc, cmul(wr, cconj(vc))));
-      }
-      __syncthreads();
+    for (int t = 0; t < TC; ++t) {
+      const int j = wp + 4 * t;
+      a[t] = (live && j < NMAX) ? A0[ri + LDA * j] : czero();
     }
-  }
-  if (tid < 32) {
-    if (lane == 0) {
-      cplx ph = cmk(1.0, 0.0);
-      S.ph[0] = ph;
-      for (int k = 0; k + 1 < n; ++k) {
-        const cplx b = A0[(k + 1) + LDA * k];
-        const double ab2 = cabs2(b);
-        double ab = 0.0;
-        if (ab2 > 1e-60) {
-          const double r = rsqrt_f64(ab2);
-          ab = ab2 * r;
-          ph = cmul(ph, cscale(b, r));
+    // columns 0 and 1 to smem (x of step 0 and c of step 0)
+#pragma unroll
+    for (int t = 0; t < TC; ++t) {
+      const int j = wp + 4 * t;
+      if (live && j == 0) S.colx[ri] = (i > 0) ? a[t] : czero();
+      if (live && j == 1) S.colc[ri] = a[t];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+#ifdef QTT_TRID_TIMING
+    tq = clock64();
+#endif
+    for (int k = 0; k + 2 < n; ++k) {
+      // ---- y = A x (partial over own columns), c_i, x_i, a0
+      cplx xi = live ? S.colx[ri] : czero();
+      const cplx ci = live ? S.colc[ri] : czero();
+      const double a0 = S.colc[k + 1].x;
+      {
+        cplx acc = czero();
+#pragma unroll
+        for (int t = 0; t < TC; ++t) {
+          const int j = wp + 4 * t;
+          if (j < NMAX) acc = cfma(a[t], S.colx[j], acc);
         }
-        S.ph[k + 1] = ph;
-        S.of[k] = ab;
-        S.e2[k] = ab * ab;
+        S.ypart[wp][i] = acc;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const cplx yi = cadd(cadd(S.ypart[0][i], S.ypart[1][i]), cadd(S.ypart[2][i], S.ypart[3][i]));
+      TS_MARK(0)
+      // ---- reflector (identical in every warp)
+      // |x|^2, Re(x^H A x) and x^H c = x^H A e_{k+1}, reduced together.  x^H c
+      // is NOT replaced by conj((A x)_{k+1}): the Gram matrices are Hermitian
+      // only to rounding, and when x is tiny against ||A|| that asymmetry is
+      // of the order of x itself (the value used is the one p = tau A v,
+      // K = tau/2 Re(v^H p) would produce).
+      double r0v = cabs2(xi), r1v = xi.x * yi.x + xi.y * yi.y;
+      double r2v = xi.x * ci.x + xi.y * ci.y, r3v = xi.x * ci.y - xi.y * ci.x;
+      const double x0r = __shfl_sync(0xffffffffu, xi.x, k + 1), x0i = __shfl_sync(0xffffffffu, xi.y, k + 1);
+      const double y0r = __shfl_sync(0xffffffffu, yi.x, k + 1), y0i = __shfl_sync(0xffffffffu, yi.y, k + 1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        r0v += __shfl_xor_sync(0xffffffffu, r0v, o);
+        r1v += __shfl_xor_sync(0xffffffffu, r1v, o);
+        r2v += __shfl_xor_sync(0xffffffffu, r2v, o);
+        r3v += __shfl_xor_sync(0xffffffffu, r3v, o);
+      }
+      const double s2 = r0v, xAx = r1v;
+      const cplx xc = cmk(r2v, r3v);
+      const double x02 = x0r * x0r + x0i * x0i;
+      const bool refl = s2 > 1e-60;
+      const bool hx0 = x02 > 1e-60;
+      const double rs = drsqrt_nr(refl ? s2 : 1.0);
+      const double r0 = drsqrt_nr(hx0 ? x02 : 1.0);
+      const double sig = s2 * rs;
+      const double ax0 = hx0 ? x02 * r0 : 0.0;
+      const cplx phs = hx0 ? cmk(x0r * r0, x0i * r0) : cmk(1.0, 0.0);
+      const cplx beta = cscale(phs, sig);
+      const double tau = refl ? drcp_nr(sig * (sig + ax0)) : 0.0;
+      const cplx vi = (i == k + 1) ? cadd(xi, beta) : xi;
+      const cplx pi = cscale(cfma(beta, ci, yi), tau);
+      // Re(v^H A v) = Re(x^H A x) + Re(beta x^H c) + Re(conj(beta) y_{k+1}) + |beta|^2 a0
+      const double vAv = xAx + (beta.x * xc.x - beta.y * xc.y) + (beta.x * y0r + beta.y * y0i) + cabs2(beta) * a0;
+      const double K = 0.5 * tau * tau * vAv;
+      const cplx wi = (live && refl) ? cmk(pi.x - K * vi.x, pi.y - K * vi.y) : czero();
+      if (wp == 0) {
+        if (live) S.hv[ri + LD * k] = vi;
+        if (i == 0) {
+          S.tau[k] = tau;
+          S.sub[k] = refl ? cmk(-beta.x, -beta.y) : cmk(x0r, x0i);   // alpha_k = T_{k+1,k}
+        }
+        __syncwarp();
+        if (i == 0) {
+          __threadfence_block();
+          *(volatile int*)&S.prog = k + 1;
+        }
+      }
+      TS_MARK(1)
+      // ---- B -= v w^H + w v^H on own columns (v_j, w_j from lane j)
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        const int j = wp + 4 * t;
+        if (j < NMAX) {
+          const cplx vj = make_double2(__shfl_sync(0xffffffffu, vi.x, j), __shfl_sync(0xffffffffu, vi.y, j));
+          const cplx wj = make_double2(__shfl_sync(0xffffffffu, wi.x, j), __shfl_sync(0xffffffffu, wi.y, j));
+          a[t] = csub(a[t], cfma_bc(vi, wj, cmul(wi, cconj(vj))));
+          // next x = column k+1 below row k+1, next c = column k+2
+          if (live && j == k + 1) S.colx[ri] = (i > k + 1) ? a[t] : czero();
+          if (live && j == k + 2) S.colc[ri] = a[t];
+        }
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      TS_MARK(2)
+    }
+    // ---- T: dg_i = A_ii, alpha_{n-2} = A_{n-1,n-2}; D = diag(ph) with
+    //      ph_{k+1} = prod_{j<=k} alpha_j / |alpha_j| (parallel prefix)
+#pragma unroll
+    for (int t = 0; t < TC; ++t) {
+      const int j = wp + 4 * t;
+      if (j < NMAX && i == j && i < n) S.dg[i] = a[t].x;
+      if (n >= 2 && j == n - 2 && i == n - 1) S.sub[n - 2] = a[t];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (wp == 0) {
+      const bool hs = i + 1 < n;
+      const cplx al = hs ? S.sub[i] : cmk(1.0, 0.0);
+      const double ab2 = cabs2(al);
+      const double r = ab2 > 1e-60 ? drsqrt_nr(ab2) : 0.0;
+      const double ab = ab2 * r;
+      cplx u = ab2 > 1e-60 ? cscale(al, r) : cmk(1.0, 0.0);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const cplx t = make_double2(__shfl_up_sync(0xffffffffu, u.x, o), __shfl_up_sync(0xffffffffu, u.y, o));
+        if (i >= o) u = cmul(t, u);
+      }
+      if (i == 0) S.ph[0] = cmk(1.0, 0.0);
+      if (hs) {
+        S.ph[i + 1] = u;
+        S.of[i] = ab;
+        S.e2[i] = ab * ab;
       }
     }
-    if (lane < n) S.dg[lane] = A0[lane + LDA * lane].x;
+#ifdef QTT_TRID_TIMING
+    if (tid == 0)
+      for (int q = 0; q < 4; ++q) S.tstep[q] = ts[q];
+#endif
+  } else if (wp == 4 && Qm) {
+    // Q_{k+1} = Q_k H_k = Q_k - tau (Q_k v) v^H, lane = row of Q
+    const int i = lane;
+    if (i < n)
+      for (int j = 0; j < n; ++j) Qm[i + LD * j] = cmk(i == j ? 1.0 : 0.0, 0.0);
+    for (int k = 0; k + 2 < n; ++k) {
+      while (*(volatile int*)&S.prog <= k) __nanosleep(32);
+      __threadfence_block();
+      const double tau = S.tau[k];
+      if (tau != 0.0 && i < n) {
+        cplx q0 = czero(), q1 = czero();
+        int j = k + 1;
+        for (; j + 1 < n; j += 2) {
+          q0 = cfma(Qm[i + LD * j], S.hv[j + LD * k], q0);
+          q1 = cfma(Qm[i + LD * (j + 1)], S.hv[j + 1 + LD * k], q1);
+        }
+        if (j < n) q0 = cfma(Qm[i + LD * j], S.hv[j + LD * k], q0);
+        const cplx sq = cscale(cadd(q0, q1), tau);
+        for (int jj = k + 1; jj < n; ++jj) {
+          cplx* q = &Qm[i + LD * jj];
+          *q = csub(*q, cmul(sq, cconj(S.hv[jj + LD * k])));
+        }
+      }
+    }
   }
   __syncthreads();
   if (tid == 0) { long long t = clock64(); S.tph[0] = t - tt0; tt0 = t; }
@@ -457,6 +486,9 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
         hi = fmax(hi, dg[i] + r);
       }
     }
+#ifdef QTT_TRID_TIMING
+    long long tb0 = clock64();
+#endif
     const double pad = 1e-14 * fmax(1.0, fmax(fabs(lo), fabs(hi)));
     lo -= pad;
     hi += pad;
@@ -480,6 +512,9 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       h = nh;
     }
     if (k < n && j == 0) S.lam[k] = 0.5 * (l + h);
+#ifdef QTT_TRID_TIMING
+    if (tid == 0) { S.tstep[3] = tb0 - tt0; S.tstep[4] = clock64() - tb0; }
+#endif
   }
   __syncthreads();
   for (int kk = tid; kk < n; kk += NT) lam_out[kk] = S.lam[n - 1 - kk] * anrm;
@@ -488,7 +523,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 }
 
 template <int NMAX, int NT>
-__device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, cplx* U_out, int LDU) {
+__device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, const cplx* Qm, cplx* U_out, int LDU) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   long long tt0 = clock64();
@@ -598,24 +633,19 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, cplx* U_out, in
   __syncthreads();
   if (tid == 0) { long long t = clock64(); S.tph[3] = t - tt0; tt0 = t; }
   if (S.bad) return false;
-  // ---- back-transformation u = Q D z: one warp per vector, lane = row
-  for (int t = wp; t < nvec; t += NT / 32) {
+  // ---- back-transformation u = Q D z with the accumulated Q (one output
+  //      element per thread)
+  for (int e = tid; e < n * nvec; e += NT) {
+    const int i = e % n, t = e / n;
     const double* z = S.Z + LD * t;
-    cplx u = (lane < n) ? cscale(S.ph[lane], z[lane]) : czero();
-    for (int k = n - 3; k >= 0; --k) {
-      const double tau = S.tau[k];
-      if (tau == 0.0) continue;
-      const cplx v = (lane > k && lane < n) ? S.hv[lane + LD * k] : czero();
-      cplx c = cfmac(v, u, czero());
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        c.x += __shfl_xor_sync(0xffffffffu, c.x, o);
-        c.y += __shfl_xor_sync(0xffffffffu, c.y, o);
-      }
-      const cplx s = cmk(c.x * tau, c.y * tau);
-      u = csub(u, cmul(v, s));
+    cplx u0 = czero(), u1 = czero();
+    int j = 0;
+    for (; j + 1 < n; j += 2) {
+      u0 = cfma(Qm[i + LD * j], cscale(S.ph[j], z[j]), u0);
+      u1 = cfma(Qm[i + LD * (j + 1)], cscale(S.ph[j + 1], z[j + 1]), u1);
     }
-    if (lane < n) U_out[lane + LDU * t] = u;
+    if (j < n) u0 = cfma(Qm[i + LD * j], cscale(S.ph[j], z[j]), u0);
+    U_out[i + LDU * t] = cadd(u0, u1);
   }
   __syncthreads();
   if (tid == 0) S.tph[4] = clock64() - tt0;
@@ -646,37 +676,6 @@ struct EigSmem {
 };
 
 
-// ---- fast reciprocal / rsqrt: one MUFU op (fp32 approx) or MUFU + Newton
-// steps to full fp64 precision (no IEEE slow-path subroutine calls)
-__device__ __forceinline__ float frsqrt_fast(float x) {
-  float y;
-  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float frcp_fast(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ double drcp_nr(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
-__device__ __forceinline__ double drsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  y = y * fma(-hx * y, y, 1.5);
-  return y;
-}
 // round-robin pair of slot k in round r (N even): circle method
 __device__ __forceinline__ void rr_pair(int N, int r, int k, int& p, int& q) {
   if (k == 0) { p = N - 1; q = r; return; }
@@ -985,20 +984,55 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
 template <int NMAX, int NT>
 __device__ void eig_values(EigSmem<NMAX>& E, int n) {
   constexpr int LD = NMAX + 1;
-  for (int e = threadIdx.x; e < n * n; e += NT) {
-    const int i = e % n, j = e / n;
-    E.A[1][i + LD * j] = E.A[0][i + LD * j];
+  for (int e = threadIdx.x; e < NMAX * NMAX; e += NT) {
+    const int i = e % NMAX, j = e / NMAX;
+    if (i < n && j < n) E.A[1][i + LD * j] = E.A[0][i + LD * j];
+    else E.A[0][i + LD * j] = czero();   // the tridiagonalisation runs on the zero-padded matrix
   }
   __syncthreads();
-  trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam);
+  trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1]);
 }
 
+#ifdef QTT_EIG_CHECK
+__device__ int g_eig_dumped = 0;
+#endif
 template <int NMAX, int NT>
 __device__ const cplx* eig_vectors(EigSmem<NMAX>& E, int n, int k, int* status) {
   constexpr int LD = NMAX + 1;
   if (k > n) k = n;
   if (k < 1) k = 1;
-  if (trid_vectors<NMAX, NT>(E.u.tr, n, k, E.V[0], LD)) return E.V[0];
+  if (trid_vectors<NMAX, NT>(E.u.tr, n, k, E.V[1], E.V[0], LD)) {
+#ifdef QTT_EIG_CHECK
+    // debug builds: residual of every returned pair against the original matrix
+    if (threadIdx.x < k) {
+      const int t = threadIdx.x;
+      double rn = 0.0, an = 0.0;
+      for (int i = 0; i < n; ++i) {
+        cplx s = czero();
+        for (int j = 0; j < n; ++j) s = cfma(E.A[1][i + LD * j], E.V[0][j + LD * t], s);
+        s = csub(s, cscale(E.V[0][i + LD * t], E.lam[t]));
+        rn += cabs2(s);
+        for (int j = 0; j < n; ++j) an += cabs2(E.A[1][i + LD * j]);
+      }
+      if (rn > 1e-20 * an + 1e-300) {
+        raise_status(status, NMAX == 16 ? 64 : (NMAX == 20 ? 128 : 256));
+        if (atomicCAS(&g_eig_dumped, 0, 1) == 0) {
+          printf("BAD n=%d k=%d t=%d rel=%g\nA=[", n, k, t, sqrt(rn / an));
+          for (int i = 0; i < n; ++i) {
+            printf("[");
+            for (int j = 0; j < n; ++j) printf("complex(%.17g,%.17g),", E.A[1][i + LD * j].x, E.A[1][i + LD * j].y);
+            printf("],\n");
+          }
+          printf("]\nlam=[");
+          for (int i = 0; i < n; ++i) printf("%.17g,", E.lam[i]);
+          printf("]\n");
+        }
+      }
+    }
+    __syncthreads();
+#endif
+    return E.V[0];
+  }
   for (int e = threadIdx.x; e < n * n; e += NT) {
     const int i = e % n, j = e / n;
     E.A[0][i + LD * j] = E.A[1][i + LD * j];

@@ -56,17 +56,36 @@ __global__ void k(double* out, long long* cyc, int iters, double a, float af) {
   c0 = clock64();
   for (int i = 0; i < iters; ++i) cv = (double)((float)cv) + 1.0;
   c1 = clock64(); if (t == 0) cyc[9] = c1 - c0;
-  out[t] = x + y + xf + r + dv + sq + sh + p + cv;
+  // __syncwarp + smem store/load round trip
+  double rt = a;
+  __shared__ double cell[32];
+  c0 = clock64();
+  for (int i = 0; i < iters; ++i) { cell[t & 31] = rt; __syncwarp(); rt = cell[(t + 1) & 31] + 1.0; __syncwarp(); }
+  c1 = clock64(); if (t == 0) cyc[10] = c1 - c0;
+  // __threadfence_block
+  c0 = clock64();
+  for (int i = 0; i < iters; ++i) { cell[t & 31] = rt + i; __threadfence_block(); }
+  c1 = clock64(); if (t == 0) cyc[11] = c1 - c0;
+  // warp_sum 5 levels (double)
+  double ws = a + t;
+  c0 = clock64();
+  for (int i = 0; i < iters / 10; ++i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+    ws *= 1e-3;
+  }
+  c1 = clock64(); if (t == 0) cyc[12] = (c1 - c0) * 10;
+  out[t] = x + y + xf + r + dv + sq + sh + p + cv + rt + ws;
 }
 int main() {
   double* out; long long* cyc; cudaMalloc(&out, 8192); cudaMalloc(&cyc, 128);
-  const char* names[] = {"DFMA", "DMUL+DADD (2 ops)", "FFMA", "MUFU.RSQ f32 + FADD", "f64 div + add", "f64 sqrt + add", "SHFL f64 + DADD", "LDS chase", "BAR.SYNC (256 thr)", "F2F d->f->d + DADD"};
+  const char* names[] = {"DFMA", "DMUL+DADD (2 ops)", "FFMA", "MUFU.RSQ f32 + FADD", "f64 div + add", "f64 sqrt + add", "SHFL f64 + DADD", "LDS chase", "BAR.SYNC (256 thr)", "F2F d->f->d + DADD", "STS+syncwarp+LDS+DADD+syncwarp", "STS+MEMBAR.CTA", "warp_sum f64 (5 lvl) + DMUL"};
   for (int nt : {32, 256}) {
     k<<<1, nt>>>(out, cyc, 1000, 1.5, 1.5f);
     cudaDeviceSynchronize();
     long long h[16]; cudaMemcpy(h, cyc, 128, cudaMemcpyDeviceToHost);
     printf("threads=%d\n", nt);
-    for (int i = 0; i < 10; ++i) printf("  %-22s %6.1f cycles/iter\n", names[i], h[i] / 1000.0);
+    for (int i = 0; i < 13; ++i) printf("  %-22s %6.1f cycles/iter\n", names[i], h[i] / 1000.0);
   }
   return 0;
 }
