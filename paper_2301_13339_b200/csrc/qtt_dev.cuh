@@ -477,21 +477,11 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       dg[i] = (i < n) ? S.dg[i] : 4.0;
       e2[i] = (i + 1 < n) ? S.e2[i] : 0.0;
     }
-    double lo = 1e300, hi = -1e300;
-#pragma unroll
-    for (int i = 0; i < NMAX; ++i) {
-      if (i < n) {
-        const double r = (i > 0 ? S.of[i - 1] : 0.0) + (i + 1 < n ? S.of[i] : 0.0);
-        lo = fmin(lo, dg[i] - r);
-        hi = fmax(hi, dg[i] + r);
-      }
-    }
 #ifdef QTT_TRID_TIMING
     long long tb0 = clock64();
 #endif
-    const double pad = 1e-14 * fmax(1.0, fmax(fabs(lo), fabs(hi)));
-    lo -= pad;
-    hi += pad;
+    // T is unitarily similar to A / ||A||_F: its spectrum lies in [-1, 1]
+    double lo = -1.0 - 1e-14, hi = 1.0 + 1e-14;
     const int gl = n <= 8 ? 32 : (n <= 16 ? 16 : 8);      // threads per eigenvalue
     const int k = tid / gl, j = tid % gl;
     const int steps = gl == 32 ? 11 : (gl == 16 ? 13 : 17);
