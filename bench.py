@@ -6,10 +6,15 @@ roofline").
 One step = one call of qtt_conv_full (Alg. 2: TT-SVD of
 f and g, QTT-FFTs, Hadamard + rounding, QTT-iFFT, expansion) over one input
 of the chosen config, inputs resident in HBM, L2 flushed between steps.
-N > 1 (torchrun): every rank runs its own independent problem (distinct
-signal seed, same kernel) — the path shards over independent problems with
-no data-path collective ("scaling": "weak"); the max over ranks of the device
-time is used.
+N > 1 (torchrun), per BASELINE.json's configs:
+  c1-c3  every rank runs its own independent problem (signal seed + rank,
+         same kernel), no data-path collective      -> "scaling": "weak"
+  c4     ONE 2^14 x 2^14 problem column-sharded over the ranks (libqtt NCCL
+         communicator: Gram allreduce per TT-SVD step, one all-gather of the
+         narrow remainder, sharded expansion)        -> "scaling": "strong"
+  c5     the 64-image batch split across the ranks, no communication
+                                                     -> "scaling": "strong"
+The max over ranks of the device time is used.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
   python bench.py --impl reference ...   # the float64 CPU oracle, same metric
@@ -35,8 +40,9 @@ from paper_2301_13339_b200 import synth  # noqa: E402
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0          # GB/s, B200_PROFILING.md fallback
-# FP64 FMA peak from unit counts (B200_PROFILING.md / DESIGN.md §6):
-# 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
+# FP64 FMA peak from unit counts: 148 SMs x 64 FP64 FMA/clk x
+# 2 flop x 1.965 GHz = 37.2 TFLOP/s (tools/probe/fp64tp.cu measured 36.1 DFMA,
+# 37.1 DMMA on this pool's B200s)
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
@@ -63,13 +69,44 @@ def workload(cfg, eps):
     return p, e, desc
 
 
-def make_inputs(cfg, rank):
+def mode_of(cfg, world):
+    if cfg == "c4" and world > 1:
+        return "sharded"
+    if synth.problem(cfg)["batch"] > 1:
+        return "batch"
+    return "independent"
+
+
+def make_inputs(cfg, rank, world=1):
+    """This rank's f (batch, or shard) and g (whole kernel, or its shard)."""
     p = synth.problem(cfg)
-    if p["batch"] > 1:
-        f = np.stack([synth.signal(cfg, index=rank * p["batch"] + i) for i in range(p["batch"])])
-    else:
+    mode = mode_of(cfg, world)
+    if mode == "batch":
+        per = p["batch"] // world
+        f = np.stack([synth.signal(cfg, index=rank * per + i) for i in range(per)])
+    elif mode == "independent":
         f = synth.signal(cfg, index=rank)
+    else:
+        raise ValueError("sharded inputs come from make_shard_inputs")
     g = synth.kernel(p["D"], p["b"], synth.CONFIGS[cfg]["w"])
+    return f, g
+
+
+def make_shard_inputs(cfg, shp, rank, world, dev):
+    """Shard `rank` of f (signal index 0) and g, generated block-wise (no
+    rank holds the global arrays); |clean| max all-reduced over the ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2301_13339_b200 import qtt as Q
+    p = synth.problem(cfg)
+    c = synth.CONFIGS[cfg]
+    (x0, y0), (bx, by) = Q.qtt_shard_geometry(shp, world, rank)
+    nx, ny = 1 << bx, 1 << by
+    cm = torch.tensor([float(np.abs(synth.clean_block(cfg, 0, x0, nx, y0, ny)).max())],
+                      dtype=torch.float64, device=dev)
+    dist.all_reduce(cm, op=dist.ReduceOp.MAX)
+    f = synth.noisy_block(cfg, 0, x0, nx, y0, ny, float(cm[0]))
+    g = synth.kernel_block(p["D"], p["b"], c["w"], x0, nx, y0, ny)
     return f, g
 
 
@@ -183,30 +220,45 @@ def run_ours(a):
     B.build()
     cfg = a.config
     p, eps, desc = workload(cfg, a.eps)
-    f, g = make_inputs(cfg, rank)
-    batch = p["batch"]
+    mode = mode_of(cfg, world)
     d = p["d"]
     n = 1 << d
     D = p["D"]
     bits = [p["b"], p["b"]] if D == 2 else [p["b"], 0]
-    shp = Q.shape(D, bits, p["layout"], batch, n, 0, n)
     dec = Q.trunc(eps, p["rmax"], p["cluster_tol"])
     fft = Q.trunc(eps, p["rhat"], p["cluster_tol"])
-    nb = Q.qtt_workspace_bytes(shp, dec, fft)
+    comm = None
+    if mode == "sharded":
+        shp = Q.shape(D, bits, p["layout"], 1)
+        uid = [Q.qtt_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = Q.qtt_comm_init(uid[0], world, rank)
+        f, g = make_shard_inputs(cfg, shp, rank, world, dev)
+        batch, n_loc = 1, n // world
+        nb = Q.qtt_comm_workspace_bytes(shp, dec, fft, comm)
+    else:
+        if mode == "batch" and p["batch"] % world:
+            raise SystemExit(f"batch {p['batch']} does not split over {world} ranks")
+        f, g = make_inputs(cfg, rank, world)
+        batch = f.shape[0] if mode == "batch" else 1
+        n_loc = n
+        shp = Q.shape(D, bits, p["layout"], batch, n, 0, n)
+        nb = Q.qtt_workspace_bytes(shp, dec, fft)
     ws = torch.empty(nb + 256, dtype=torch.uint8, device=dev)
     f_d = torch.from_numpy(np.ascontiguousarray(f).reshape(-1)).to(dev)
     g_d = torch.from_numpy(np.ascontiguousarray(g).reshape(-1)).to(dev)
-    y_d = torch.empty(batch * n, dtype=torch.float64, device=dev)
+    y_d = torch.empty(batch * n_loc, dtype=torch.float64, device=dev)
     f_h = torch.from_numpy(np.ascontiguousarray(f).reshape(-1)).pin_memory()
     g_h = torch.from_numpy(np.ascontiguousarray(g).reshape(-1)).pin_memory()
-    y_h = torch.empty(batch * n, dtype=torch.float64).pin_memory()
+    y_h = torch.empty(batch * n_loc, dtype=torch.float64).pin_memory()
+    del f, g
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 
     def step():
         Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, dec, fft, p["shift"],
-                        p["scale"], ws.data_ptr(), nb, sp)
+                        p["scale"], ws.data_ptr(), nb, sp, comm=comm)
 
     def e2e_step():
         f_d.copy_(f_h, non_blocking=True)
@@ -233,7 +285,7 @@ def run_ours(a):
 
     # correctness guard of this run: numeric status + ranks
     rep = Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, dec, fft, p["shift"],
-                          p["scale"], ws.data_ptr(), nb, sp, report=True)
+                          p["scale"], ws.data_ptr(), nb, sp, report=True, comm=comm)
     for _ in range(a.warmup):
         step()
     barrier()
@@ -264,12 +316,14 @@ def run_ours(a):
         t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ms_e2e = float(t[0]), float(t[1])
-    el_step = batch * n
-    total_el = world * el_step * a.steps
+    el_step = batch * n_loc                    # elements this rank outputs per step
+    total_el = world * el_step * a.steps       # whole job (all ranks)
     value = total_el / (ms / 1e3)
     e2e = total_el / (ms_e2e / 1e3)
 
     if rank != 0:
+        if comm is not None:
+            comm.close()
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
@@ -277,9 +331,9 @@ def run_ours(a):
     hbm, src = peaks()
     ng = 1
     nf = batch
-    # algorithmic bytes per stage: TT-SVD two-read floor 16 B/el per
-    # input; expansion 8 B/el written
-    alg = {"ttsvd": ("hbm", 16.0 * n * (nf + ng)), "expand": ("hbm", 8.0 * n * nf)}
+    # algorithmic bytes per stage and rank: TT-SVD two-read floor
+    # 16 B/el per input; expansion 8 B/el written
+    alg = {"ttsvd": ("hbm", 16.0 * n_loc * (nf + ng)), "expand": ("hbm", 8.0 * n_loc * nf)}
     cf = chain_flops(d, p["rhat"])
     for k in cf:
         alg[k] = ("alu", float(cf[k]) * (nf if k != "qfft" else (nf + ng) / 2))
@@ -302,15 +356,20 @@ def run_ours(a):
             gbs = alg[k][1] / (stages[k] / 1e3) / 1e9
             passes[k] = {"ms": round(stages[k], 4), "alg_GBps": round(gbs, 1),
                          "frac_hbm": round(gbs / hbm, 4)}
+    par = {"independent": f"independent problems x{world}",
+           "batch": f"batch of {p['batch']} split {world} ways ({batch} images/GPU), no communication",
+           "sharded": f"one problem column-sharded {world} ways (NCCL Gram allreduce + W all-gather)"}[mode]
     line = {
         "metric": "end-to-end full-array elements/s (decompose+QTT conv+expand), fraction of HBM roofline",
         "value": value, "unit": "elements/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "weak" if mode == "independent" else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded SAR-like scatterers + sinc kernel, BASELINE.json configs)",
-        "config": {"workload": desc, "global_batch": world * batch, "elements_per_step": el_step,
-                   "parallelism": f"independent problems x{world}" if world > 1 else "single GPU",
+        "config": {"workload": desc, "global_batch": (world * batch if mode != "sharded" else 1),
+                   "elements_per_step": el_step * world,
+                   "parallelism": par if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MiB write)"},
-        "hbm_fraction_e2e_floor": (40.0 * el_step * world / (ms / 1e3 / a.steps) / 1e9) / hbm,
+        "hbm_fraction_e2e_floor": (40.0 * el_step * world / (ms / 1e3 / a.steps) / 1e9) / (hbm * world),
         "e2e": {"value": e2e, "unit": "elements/s",
                 "h2d_bytes_per_step": int(f_h.numel() * 8 + g_h.numel() * 8),
                 "d2h_bytes_per_step": int(y_h.numel() * 8)},
@@ -323,8 +382,16 @@ def run_ours(a):
         "status_bits": rep["status_bits"],
     }
     if not a.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = oracle_run(cfg, eps, a.cpu_seconds)
+        if d <= 24:
+            line["cpu_baseline"] = oracle_run(cfg, eps, a.cpu_seconds)
+        else:
+            line["cpu_baseline"] = {"value": None, "unit": "elements/s", "kind": "oracle",
+                                    "cores": len(os.sched_getaffinity(0)),
+                                    "sample": "skipped: one oracle pipeline at d = 28 takes minutes "
+                                              "(SURVEY F15), beyond the bounded-sample budget"}
     print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -95,6 +95,60 @@ def signal(name, index=0, noisy=True):
     return clean + sigma * rng.standard_normal((n, n))
 
 
+def _scatterers(name, index):
+    """Draws of a 2D config in the order of signal(): positions, amplitudes;
+    returns (rng positioned before the noise draw, xs, ys, amp)."""
+    c = CONFIGS[name]
+    rng = np.random.Generator(np.random.PCG64(c["seed"] + index))
+    S = c["S"]
+    xs = rng.uniform(-0.8, 0.8, S)
+    ys = rng.uniform(-0.8, 0.8, S)
+    amp = rng.uniform(0.5, 1.0, S)
+    return rng, xs, ys, amp
+
+
+def clean_block(name, index, x0, nx, y0, ny):
+    """Rows y0..y0+ny-1, columns x0..x0+nx-1 of the clean 2D image of
+    signal(name, index, noisy=False) (same arithmetic, restricted)."""
+    c = CONFIGS[name]
+    _, xs, ys, amp = _scatterers(name, index)
+    x, _ = grid(c["b"])
+    U = sinc(c["w"] * (x[y0:y0 + ny, None] - ys[None, :]))
+    V = sinc(c["w"] * (x[x0:x0 + nx, None] - xs[None, :]))
+    return (U * amp[None, :]) @ V.T
+
+
+def noisy_block(name, index, x0, nx, y0, ny, clean_max, row_chunk=256):
+    """The same block of signal(name, index): clean_block plus the noise
+    of the full image's row-major standard_normal stream (drawn in row
+    chunks up to the block's last row; sigma = sigma_rel * clean_max, with
+    clean_max the maximum of |clean| over the WHOLE image)."""
+    c = CONFIGS[name]
+    n = 1 << c["b"]
+    rng, _, _, _ = _scatterers(name, index)
+    out = clean_block(name, index, x0, nx, y0, ny)
+    sigma = c["sigma"] * float(clean_max)
+    r = 0
+    while r < y0 + ny:
+        m = min(row_chunk, y0 + ny - r)
+        z = rng.standard_normal((m, n))
+        lo, hi = max(r, y0), min(r + m, y0 + ny)
+        if lo < hi:
+            out[lo - y0:hi - y0] += sigma * z[lo - r:hi - r, x0:x0 + nx]
+        r += m
+    return out
+
+
+def kernel_block(D, b, w, x0, nx, y0=0, ny=1):
+    """Block of kernel(D, b, w) (rows y0.., columns x0..; 1D: x0..x0+nx)."""
+    x, dx = grid(b)
+    g1 = sinc(w * x)
+    tot = g1.sum() if D == 1 else g1.sum() ** 2
+    if D == 1:
+        return g1[x0:x0 + nx] / (dx * tot)
+    return np.outer(g1[y0:y0 + ny], g1[x0:x0 + nx]) / (dx * dx * tot)
+
+
 def problem(name):
     """Shape / truncation parameters of a config (caps from Q4)."""
     c = CONFIGS[name]

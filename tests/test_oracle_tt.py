@@ -182,3 +182,20 @@ def test_maxrank1_residual_is_sigma2():
     v = A.reshape(-1, order="F")
     C = O.tt_svd(v, 0.0, 1)
     assert np.linalg.norm(O.full(C) - v) == pytest.approx(1.0, rel=1e-14)
+
+
+def test_synth_blocks_reproduce_the_global_arrays():
+    """Shard-wise input generation (multi-GPU bench) = slices of the global
+    signal / kernel (same draws, same arithmetic)."""
+    from paper_2301_13339_b200 import synth
+    full = synth.signal("c2")
+    clean = synth.signal("c2", noisy=False)
+    cm = np.abs(clean).max()
+    for (x0, nx, y0, ny) in [(0, 512, 0, 256), (0, 512, 256, 256), (256, 256, 256, 256), (128, 64, 300, 17)]:
+        blk = synth.noisy_block("c2", 0, x0, nx, y0, ny, cm, row_chunk=100)
+        np.testing.assert_allclose(blk, full[y0:y0 + ny, x0:x0 + nx], rtol=0, atol=1e-12)
+    g = synth.kernel(2, 9, 60.0)
+    np.testing.assert_allclose(synth.kernel_block(2, 9, 60.0, 256, 256, 0, 256), g[0:256, 256:512],
+                               rtol=1e-14, atol=0)
+    g1 = synth.kernel(1, 12, 40.0)
+    np.testing.assert_allclose(synth.kernel_block(1, 12, 40.0, 1024, 1024), g1[1024:2048], rtol=1e-14)
