@@ -166,6 +166,7 @@ struct TridSmem {
   cplx colx[32];             // next reflector column (rows below the diagonal)
   cplx colc[32];             // the column after it
   cplx ypart[4][32];         // per-warp partial A x
+  double red4[4];            // the four reduced sums of a reflector
   cplx ph[NMAX];             // D = diag(ph)
   double tau[NMAX];
   double dg[NMAX];           // diag of T (normalised)
@@ -178,7 +179,6 @@ struct TridSmem {
   long long tstep[5];        // clock64 per tridiagonalisation sub-phase (diagnostics)
   double anrm;
   int bad;
-  int prog;                  // reflectors published by the tridiagonalising warp
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -224,20 +224,19 @@ __device__ __forceinline__ float frcp_fast(float x) {
   return y;
 }
 __device__ __forceinline__ double drcp_nr(double x) {
+  // MUFU seed ~1e-6 relative; two Newton steps reach < 1 ulp (tools/probe/newton.cu)
   double y;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   double e = fma(-x, y, 1.0);
   y = fma(y, e, y);
   e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
   return fma(y, e, y);
 }
 __device__ __forceinline__ double drsqrt_nr(double x) {
+  // MUFU seed ~1e-6 relative; two Newton steps reach ~1 ulp (tools/probe/newton.cu)
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double hx = 0.5 * x;
-  y = y * fma(-hx * y, y, 1.5);
   y = y * fma(-hx * y, y, 1.5);
   y = y * fma(-hx * y, y, 1.5);
   return y;
@@ -248,20 +247,23 @@ __device__ __forceinline__ double drsqrt_nr(double x) {
 // of the normalised T, |lambda| <= ||T||_F = 1) so every loop runs
 // unpredicated: the padding adds no sign change for x < 4 and no eigenvector
 // component.
-template <int NMAX>
+// L <= NMAX: only the first L entries are visited (callers pick the smallest
+// L >= n; entries n..L-1 are the padding).
+template <int NMAX, int L = NMAX>
 __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const double (&e2)[NMAX], double x) {
+  static_assert(L <= NMAX, "L <= NMAX");
   double p0 = 1.0, p1 = dg[0] - x;
   unsigned s1 = (unsigned)__double2hiint(p1) >> 31;      // sign bits (integer pipe)
   int cnt = (int)s1;
 #pragma unroll
-  for (int i = 1; i < NMAX; ++i) {
+  for (int i = 1; i < L; ++i) {
     const double p2 = fma(dg[i] - x, p1, -e2[i - 1] * p0);
     const unsigned s2 = (unsigned)__double2hiint(p2) >> 31;
     cnt += (int)(s1 ^ s2);
     s1 = s2;
     p0 = p1;
     p1 = p2;
-    if ((i & 7) == 7 && i + 1 < NMAX) {
+    if ((i & 7) == 7 && i + 1 < L) {
       const double a = fabs(p1) + fabs(p0);
       const double sc = a > 1e120 ? 1e-120 : (a < 1e-120 ? 1e120 : 1.0);
       p0 *= sc;
@@ -285,13 +287,12 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     const int i = e % n, j = e / n;
     A0[i + LDA * j] = cscale(A0[i + LDA * j], inv);
   }
-  if (tid == 0) { S.bad = 0; S.anrm = anrm; S.prog = 0; }
+  if (tid == 0) { S.bad = 0; S.anrm = anrm; }
   __syncthreads();
   long long tt0 = clock64();
-  // ---- Householder tridiagonalisation by warp 0 alone (lane = row, no CTA
-  //      barriers); warp 1 accumulates Q = H_0 H_1 ... H_{n-3} explicitly in
-  //      Qm as the reflectors appear (S.prog), so the back-transformation is
-  //      a plain product.
+  // ---- Householder tridiagonalisation by warps 0-3 (named barriers 1/2);
+  //      warp 4 accumulates Q = H_0 H_1 ... H_{n-3} explicitly in Qm one step
+  //      behind, so the back-transformation is a plain product.
   const int wp = tid >> 5;
 #ifdef QTT_TRID_TIMING
   long long ts[4] = {0, 0, 0, 0}, tq = 0;
@@ -339,7 +340,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #pragma unroll
         for (int t = 0; t < TC; ++t) {
           const int j = wp + 4 * t;
-          if (j < NMAX) acc = cfma(a[t], S.colx[j], acc);
+          if (j > k && j < n) acc = cfma(a[t], S.colx[j], acc);   // x_j = 0 elsewhere (warp-uniform test)
         }
         S.ypart[wp][i] = acc;
       }
@@ -352,22 +353,29 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       // only to rounding, and when x is tiny against ||A|| that asymmetry is
       // of the order of x itself (the value used is the one p = tau A v,
       // K = tau/2 Re(v^H p) would produce).
-      double r0v = cabs2(xi), r1v = xi.x * yi.x + xi.y * yi.y;
-      double r2v = xi.x * ci.x + xi.y * ci.y, r3v = xi.x * ci.y - xi.y * ci.x;
+      //      (warp w reduces the w-th of the four sums; exchanged via smem)
+      {
+        double rv = wp == 0 ? cabs2(xi)
+                  : wp == 1 ? xi.x * yi.x + xi.y * yi.y
+                  : wp == 2 ? xi.x * ci.x + xi.y * ci.y
+                            : xi.x * ci.y - xi.y * ci.x;
+#pragma unroll
+        for (int o = (NMAX <= 16 ? 8 : 16); o > 0; o >>= 1) rv += __shfl_xor_sync(0xffffffffu, rv, o);
+        if (i == 0) S.red4[wp] = rv;
+      }
       const double x0r = __shfl_sync(0xffffffffu, xi.x, k + 1), x0i = __shfl_sync(0xffffffffu, xi.y, k + 1);
       const double y0r = __shfl_sync(0xffffffffu, yi.x, k + 1), y0i = __shfl_sync(0xffffffffu, yi.y, k + 1);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        r0v += __shfl_xor_sync(0xffffffffu, r0v, o);
-        r1v += __shfl_xor_sync(0xffffffffu, r1v, o);
-        r2v += __shfl_xor_sync(0xffffffffu, r2v, o);
-        r3v += __shfl_xor_sync(0xffffffffu, r3v, o);
-      }
-      const double s2 = r0v, xAx = r1v;
-      const cplx xc = cmk(r2v, r3v);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      TS_MARK(1)
+      const double s2 = S.red4[0], xAx = S.red4[1];
+      const cplx xc = cmk(S.red4[2], S.red4[3]);
       const double x02 = x0r * x0r + x0i * x0i;
+      // reflect when the column is above 1e-30 ||A|| (below that it is
+      // treated as reduced); the phase of x0 is needed whenever |x0|^2 is a
+      // normal number: tau = 1 / (sig (sig + |x0|)) is only unitary with the
+      // true |x0| (a 1e-60 cut here broke columns with |x0| ~ 1e-3 |x|)
       const bool refl = s2 > 1e-60;
-      const bool hx0 = x02 > 1e-60;
+      const bool hx0 = x02 > 1e-300;
       const double rs = drsqrt_nr(refl ? s2 : 1.0);
       const double r0 = drsqrt_nr(hx0 ? x02 : 1.0);
       const double sig = s2 * rs;
@@ -381,24 +389,22 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       const double vAv = xAx + (beta.x * xc.x - beta.y * xc.y) + (beta.x * y0r + beta.y * y0i) + cabs2(beta) * a0;
       const double K = 0.5 * tau * tau * vAv;
       const cplx wi = (live && refl) ? cmk(pi.x - K * vi.x, pi.y - K * vi.y) : czero();
+      // reflector k for the Q warp: ordered by the end-of-step barrier 2
       if (wp == 0) {
         if (live) S.hv[ri + LD * k] = vi;
         if (i == 0) {
           S.tau[k] = tau;
           S.sub[k] = refl ? cmk(-beta.x, -beta.y) : cmk(x0r, x0i);   // alpha_k = T_{k+1,k}
         }
-        __syncwarp();
-        if (i == 0) {
-          __threadfence_block();
-          *(volatile int*)&S.prog = k + 1;
-        }
       }
-      TS_MARK(1)
+      TS_MARK(2)
       // ---- B -= v w^H + w v^H on own columns (v_j, w_j from lane j)
 #pragma unroll
       for (int t = 0; t < TC; ++t) {
         const int j = wp + 4 * t;
-        if (j < NMAX) {
+        // finished columns (j <= k) are never read again, padding (j >= n)
+        // stays zero: both skipped (warp-uniform test)
+        if (j > k && j < n) {
           const cplx vj = make_double2(__shfl_sync(0xffffffffu, vi.x, j), __shfl_sync(0xffffffffu, vi.y, j));
           const cplx wj = make_double2(__shfl_sync(0xffffffffu, wi.x, j), __shfl_sync(0xffffffffu, wi.y, j));
           a[t] = csub(a[t], cfma_bc(vi, wj, cmul(wi, cconj(vj))));
@@ -407,8 +413,9 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
           if (live && j == k + 2) S.colc[ri] = a[t];
         }
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      TS_MARK(2)
+      // end of step: warps 0-3 and the Q warp (160 threads)
+      asm volatile("bar.sync 2, 160;" ::: "memory");
+      TS_MARK(3)
     }
     // ---- T: dg_i = A_ii, alpha_{n-2} = A_{n-1,n-2}; D = diag(ph) with
     //      ph_{k+1} = prod_{j<=k} alpha_j / |alpha_j| (parallel prefix)
@@ -441,15 +448,16 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #ifdef QTT_TRID_TIMING
     if (tid == 0)
       for (int q = 0; q < 4; ++q) S.tstep[q] = ts[q];
+    if (tid == 0) S.tph[4] = 0;
 #endif
-  } else if (wp == 4 && Qm) {
-    // Q_{k+1} = Q_k H_k = Q_k - tau (Q_k v) v^H, lane = row of Q
+  } else if (wp == 4) {
+    // Q_{k+1} = Q_k H_k = Q_k - tau (Q_k v) v^H, lane = row of Q; reflector
+    // k is read after the end-of-step barrier of step k (one step behind)
     const int i = lane;
     if (i < n)
       for (int j = 0; j < n; ++j) Qm[i + LD * j] = cmk(i == j ? 1.0 : 0.0, 0.0);
     for (int k = 0; k + 2 < n; ++k) {
-      while (*(volatile int*)&S.prog <= k) __nanosleep(32);
-      __threadfence_block();
+      asm volatile("bar.sync 2, 160;" ::: "memory");
       const double tau = S.tau[k];
       if (tau != 0.0 && i < n) {
         cplx q0 = czero(), q1 = czero();
@@ -492,7 +500,12 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     const unsigned gmask = (gl == 32) ? 0xffffffffu : (((1u << gl) - 1u) << base);
     for (int st = 0; st < steps; ++st) {
       const double x = l + (h - l) * sj;
-      const int c = (k < n) ? sturm_count<NMAX>(dg, e2, x) : 0;
+      int c = 0;
+      if (k < n) {
+        if (NMAX > 8 && n <= 8) c = sturm_count<NMAX, (NMAX > 8 ? 8 : NMAX)>(dg, e2, x);
+        else if (NMAX > 16 && n <= 16) c = sturm_count<NMAX, (NMAX > 16 ? 16 : NMAX)>(dg, e2, x);
+        else c = sturm_count<NMAX>(dg, e2, x);
+      }
       const unsigned bal = __ballot_sync(0xffffffffu, c >= k + 1) & gmask;
       const int first = bal ? (__ffs(bal) - 1 - base) : gl;
       const double w = h - l;
@@ -503,7 +516,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     }
     if (k < n && j == 0) S.lam[k] = 0.5 * (l + h);
 #ifdef QTT_TRID_TIMING
-    if (tid == 0) { S.tstep[3] = tb0 - tt0; S.tstep[4] = clock64() - tb0; }
+    if (tid == 0) { S.tstep[4] = clock64() - tb0; }
 #endif
   }
   __syncthreads();

@@ -99,3 +99,27 @@ def test_nearly_diagonal_gram_with_rounding_asymmetry(n, mode):
     k = n if mode == 0 else 2
     # backward-stable to ~1e-13 ||K|| even where a pair is split by only ~eps ||K||
     assert np.linalg.norm(H @ ug[:, :k] - ug[:, :k] * lg[:k]) <= 1e-12 * nrm
+
+
+def test_reflector_column_with_tiny_leading_entry():
+    """A Gram from the rounding of a low-rank convolution (captured input;
+    expected values from LAPACK): the first reflector column has |x_0| ~
+    2e-3 |x| with |x|^2 ~ 4e-57 ||A||^2.  tau = 1/(sig (sig + |x_0|)) must use
+    the true |x_0| or the reflector is not unitary (regression)."""
+    A = np.array([
+        [1531223873305724.5 + 0.030530668773954436j, -3.0459277739610207e-16 + 1.5869363548134762e-16j,
+         6.3977605118900718e-16 - 7.8462981843276434e-16j, 1.3105847166115026e-13 - 3.3426406628489761e-14j],
+        [-3.0459277739610202e-16 - 1.5869363548134792e-16j, 1.1180514300345477e-44 + 7.3921320910909081e-61j,
+         -1.1583067596956201e-44 - 9.3951900008114141e-46j, -2.0880786016810227e-16 - 4.1180467773050174e-15j],
+        [6.3977605118900709e-16 + 7.8462981843276425e-16j, -1.1583067596956201e-44 + 9.3951900008114001e-46j,
+         1.2416893482199729e-44 + 7.2213845986493022e-61j, 5.9564751273308451e-16 + 4.199201165122222e-15j],
+        [1.5808276109183045e-13 + 3.0227753260396385e-14j, -2.0880786016810259e-16 + 4.1180467773050182e-15j,
+         5.9564751273308471e-16 - 4.1992011651222228e-15j, 1531223873305665 + 0.043046907873092941j]])
+    H = 0.5 * (A + A.conj().T)
+    lw = np.linalg.eigvalsh(H)[::-1]
+    nrm = np.linalg.norm(A)
+    for mode in (0, 3):
+        lg, ug, _ = _gpu_eigh(A, mode)
+        assert np.max(np.abs(lg - lw)) <= 1e-14 * nrm
+        k = 4 if mode == 0 else 2
+        assert np.linalg.norm(H @ ug[:, :k] - ug[:, :k] * lg[:k]) <= 1e-12 * nrm

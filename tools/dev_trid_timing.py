@@ -14,4 +14,4 @@ for n in (16, 20):
     for _ in range(3): Q.qtt_debug_eigh(a.data_ptr(), n, lam.data_ptr(), U.data_ptr(), sw.data_ptr(), s, mode=0)
     torch.cuda.synchronize()
     v = sw.cpu().numpy()
-    print(f"n={n}: phases(trid, values, twist, mgs, back)={list(v[2:7])} trid sub(y, reflector, update, values-init, values-loop)={list(v[7:12])}")
+    print(f"n={n}: phases(trid, values, twist, mgs, back)={list(v[2:7])} trid sub(y+bar, reduce+bar, scalars+publish, update+bar, values-loop)={list(v[7:12])}")
