@@ -173,20 +173,22 @@ __device__ void write_core_from_U(const DecProb& pr, int k, const cplx* U, int l
   if (threadIdx.x == 0) pr.ranks[k] = rk;
 }
 
+template <int NE>
 struct LevelSolveSmem {
-  EigSmem<32> E;
+  EigSmem<NE> E;
   double G[1024];
   double P[2][32 * 16];
   double PT[1024];
   int rk;
 };
 
+template <int NE>
 __global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nblk, DecParams prm) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
-  LevelSolveSmem& S = *reinterpret_cast<LevelSolveSmem*>(smraw);
+  LevelSolveSmem<NE>& S = *reinterpret_cast<LevelSolveSmem<NE>*>(smraw);
   const int tid = threadIdx.x;
-  constexpr int LD = EigSmem<32>::LD;
+  constexpr int LD = EigSmem<NE>::LD;
   for (int e = tid; e < 1024; e += NT) {
     double s = 0.0;
     if (nblk == 0) s = pr.gsum[e];   // Gram already reduced (across shards)
@@ -228,14 +230,14 @@ __global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nb
       S.E.A[0][i + LD * j] = cmk(s, 0.0);
     }
     __syncthreads();
-    eig_values<32, NT>(S.E, rr);
+    eig_values<NE, NT>(S.E, rr);
     if (tid == 0) {
       int mp = rr < (1 << (d - k)) ? rr : (1 << (d - k));
       S.rk = rank_rule(S.E.lam, mp, tau2, prm.rmax, prm.ctol);
     }
     __syncthreads();
     const int rk = S.rk;
-    const cplx* U = eig_vectors<32, NT>(S.E, rr, rk, prm.status);
+    const cplx* U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
     write_core_from_U(pr, k, U, LD, rr, rk);
     // P_k[a][r] = sum_rho P_{k-1}[a mod h][rho] U[rho + r_prev (a div h)][r]
     double* Pn = S.P[cur ^ 1];
@@ -376,16 +378,18 @@ __global__ void __launch_bounds__(NT) k_project(const DecProb* probs, int k, int
 }
 
 // ------------------------------------------------------------------- K2'
+template <int NE>
 struct StepSolveSmem {
-  EigSmem<32> E;
+  EigSmem<NE> E;
   int rk;
 };
 
+template <int NE>
 __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, int nblk, DecParams prm) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
-  StepSolveSmem& S = *reinterpret_cast<StepSolveSmem*>(smraw);
-  constexpr int LD = EigSmem<32>::LD;
+  StepSolveSmem<NE>& S = *reinterpret_cast<StepSolveSmem<NE>*>(smraw);
+  constexpr int LD = EigSmem<NE>::LD;
   const int tid = threadIdx.x;
   const int r_prev = pr.ranks[k - 1], rr = 2 * r_prev;
   for (int e = tid; e < rr * rr; e += NT) {
@@ -396,14 +400,14 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
     S.E.A[0][i + LD * j] = cmk(s, 0.0);
   }
   __syncthreads();
-  eig_values<32, NT>(S.E, rr);
+  eig_values<NE, NT>(S.E, rr);
   if (tid == 0) {
     int mp = rr < (1 << (pr.d - k)) ? rr : (1 << (pr.d - k));
     S.rk = rank_rule(S.E.lam, mp, *pr.tau2, prm.rmax, prm.ctol);
   }
   __syncthreads();
   const int rk = S.rk;
-  const cplx* U = eig_vectors<32, NT>(S.E, rr, rk, prm.status);
+  const cplx* U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
   write_core_from_U(pr, k, U, LD, rr, rk);
   for (int e = tid; e < rr * rk; e += NT) {
     int a = e % rr, r = e / rr;
@@ -416,9 +420,10 @@ static constexpr int FIN_CAP = 4096;             // doubles of W_{k-1} the finis
 static constexpr int FIN_COLS = FIN_CAP / RC;     // 256 columns at the rank cap
 static_assert(FIN_COLS == FIN_COLS_HOST, "host driver mirrors FIN_COLS");
 static constexpr int FIN_D = 12;                  // d <= 12: whole TT-SVD in one CTA
+template <int NE>
 struct FinishSmem {
   double B[2][FIN_CAP];
-  EigSmem<32> E;
+  EigSmem<NE> E;
   double G[1024];
   int rk;
 };
@@ -446,12 +451,13 @@ __device__ void gram_smem(const double* M, int rows, int n, double* scratch, dou
   gram_reduce_cta<4>(acc, scratch, G);
 }
 
+template <int NE>
 __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart, int src_is_a,
                                                DecParams prm) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
-  FinishSmem& S = *reinterpret_cast<FinishSmem*>(smraw);
-  constexpr int LD = EigSmem<32>::LD;
+  FinishSmem<NE>& S = *reinterpret_cast<FinishSmem<NE>*>(smraw);
+  constexpr int LD = EigSmem<NE>::LD;
   const int tid = threadIdx.x;
   const int d = pr.d;
   int r_prev;
@@ -490,14 +496,14 @@ __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart,
       S.E.A[0][i + LD * j] = cmk(S.G[i * 32 + j], 0.0);
     }
     __syncthreads();
-    eig_values<32, NT>(S.E, rr);
+    eig_values<NE, NT>(S.E, rr);
     if (tid == 0) {
       int mp = rr < n ? rr : n;
       S.rk = rank_rule(S.E.lam, mp, tau2, prm.rmax, prm.ctol);
     }
     __syncthreads();
     const int rk = S.rk;
-    const cplx* U = eig_vectors<32, NT>(S.E, rr, rk, prm.status);
+    const cplx* U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
     write_core_from_U(pr, k, U, LD, rr, rk);
     // W_k = U_r^T M_k
     const double* M = S.B[cur];
@@ -519,10 +525,12 @@ __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart,
 }
 
 size_t smem_level_gram() { return 2 * CHUNK_SMEM * sizeof(double); }
-size_t smem_level_solve() { return sizeof(LevelSolveSmem); }
+template <int NE> size_t smem_level_solve() { return sizeof(LevelSolveSmem<NE>); }
 size_t smem_project() { return sizeof(ProjSmem); }
-size_t smem_step_solve() { return sizeof(StepSolveSmem); }
-size_t smem_finish() { return sizeof(FinishSmem); }
+template <int NE> size_t smem_step_solve() { return sizeof(StepSolveSmem<NE>); }
+template <int NE> size_t smem_finish() { return sizeof(FinishSmem<NE>); }
+// solver width: 2 r_{k-1} <= 2 R_max rows; 20 covers R_max <= 10 (all configs)
+static inline bool narrow(const DecParams& prm) { return prm.rmax <= 10; }
 
 // ------------------------------------------------- sharded-path helpers
 // gsum_t = sum over the tensor's local shards j (in order) of sum over the
@@ -591,13 +599,15 @@ cudaError_t launch_gram_reduce(const DecProb* sh, int ntens, int nlocal, int nbl
 }
 
 cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st) {
-  k_level_solve<<<dim3(1, ntens), NT, smem_level_solve(), st>>>(tn, nblk, prm);
+  if (narrow(prm)) k_level_solve<20><<<dim3(1, ntens), NT, smem_level_solve<20>(), st>>>(tn, nblk, prm);
+  else k_level_solve<32><<<dim3(1, ntens), NT, smem_level_solve<32>(), st>>>(tn, nblk, prm);
   count_launches(1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st) {
-  k_step_solve<<<dim3(1, ntens), NT, smem_step_solve(), st>>>(tn, k, nblk, prm);
+  if (narrow(prm)) k_step_solve<20><<<dim3(1, ntens), NT, smem_step_solve<20>(), st>>>(tn, k, nblk, prm);
+  else k_step_solve<32><<<dim3(1, ntens), NT, smem_step_solve<32>(), st>>>(tn, k, nblk, prm);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -611,7 +621,8 @@ cudaError_t launch_project(bool from_x, const DecProb* pr, int nprob, int k, int
 }
 
 cudaError_t launch_finish(const DecProb* tn, int ntens, int k, int src_is_a, DecParams prm, cudaStream_t st) {
-  k_finish<<<dim3(1, ntens), NT, smem_finish(), st>>>(tn, k, src_is_a, prm);
+  if (narrow(prm)) k_finish<20><<<dim3(1, ntens), NT, smem_finish<20>(), st>>>(tn, k, src_is_a, prm);
+  else k_finish<32><<<dim3(1, ntens), NT, smem_finish<32>(), st>>>(tn, k, src_is_a, prm);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -636,35 +647,29 @@ cudaError_t setup_ttsvd_kernels() {
   if ((e = cudaFuncSetAttribute(k_level_gram, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_level_gram())))
     return e;
-  if ((e = cudaFuncSetAttribute(k_level_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_level_solve())))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_project<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_project())))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_project<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_project())))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_step_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_step_solve())))
-    return e;
-  if ((e = cudaFuncSetAttribute(k_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_finish())))
-    return e;
+#define QTT_SET_SMEM(K, BYTES) \
+  if ((e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(BYTES)))) return e;
+  QTT_SET_SMEM(k_level_solve<20>, smem_level_solve<20>())
+  QTT_SET_SMEM(k_level_solve<32>, smem_level_solve<32>())
+  QTT_SET_SMEM(k_project<true>, smem_project())
+  QTT_SET_SMEM(k_project<false>, smem_project())
+  QTT_SET_SMEM(k_step_solve<20>, smem_step_solve<20>())
+  QTT_SET_SMEM(k_step_solve<32>, smem_step_solve<32>())
+  QTT_SET_SMEM(k_finish<20>, smem_finish<20>())
+  QTT_SET_SMEM(k_finish<32>, smem_finish<32>())
+#undef QTT_SET_SMEM
   return cudaSuccess;
 }
 
 // Launch the whole TT-SVD for nprob problems of equal d (device array probs).
 cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st) {
   if (d <= FIN_D) {
-    k_finish<<<dim3(1, nprob), NT, smem_finish(), st>>>(probs_dev, 1, 1, prm);
-    count_launches(1);
-    return cudaGetLastError();
+    return launch_finish(probs_dev, nprob, 1, 1, prm, st);
   }
   const int nblk = dec_nblk(d);
   k_level_gram<<<dim3(nblk, nprob), NT, smem_level_gram(), st>>>(probs_dev, nblk, prm.status);
-  k_level_solve<<<dim3(1, nprob), NT, smem_level_solve(), st>>>(probs_dev, nblk, prm);
-  count_launches(2);
+  count_launches(1);
+  launch_level_solve(probs_dev, nprob, nblk, prm, st);
   // K3: W_m from x, Gram for step m+1
   int k = LVL_M;
   {
@@ -677,17 +682,16 @@ cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams p
     ++k;
     // steps while W_{k-1} has more than FIN_COLS columns
     while ((1 << (d - k + 1)) > FIN_COLS) {
-      k_step_solve<<<dim3(1, nprob), NT, smem_step_solve(), st>>>(probs_dev, k, prev_nb, prm);
+      launch_step_solve(probs_dev, nprob, k, prev_nb, prm, st);
       uint64_t nc = (1ull << (d - k)) / 128;
       int nb2 = (int)(nc < (uint64_t)NBLK_MAX ? nc : (uint64_t)NBLK_MAX);
       k_project<false><<<dim3(nb2, nprob), NT, smem_project(), st>>>(probs_dev, k, nb2, src_is_a);
-      count_launches(2);
+      count_launches(1);
       src_is_a ^= 1;
       prev_nb = nb2;
       ++k;
     }
-    k_finish<<<dim3(1, nprob), NT, smem_finish(), st>>>(probs_dev, k, src_is_a, prm);
-    count_launches(1);
+    launch_finish(probs_dev, nprob, k, src_is_a, prm, st);
   }
   return cudaGetLastError();
 }
