@@ -505,19 +505,19 @@ qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, c
                       "copy descriptors")))
     return r;
   const int d = D.d, dl = D.dl, nsh = (int)D.sh.size();
-  int nblk = dec_nblk_loc(dl);
+  int nblk = dec_nblk_loc(dl, nsh);
   if ((r = cuda_check(launch_level_gram(D.sh_dev, nsh, nblk, prm.status, st), "level gram"))) return r;
   if ((r = reduce_grams(D, comm, nblk, st))) return r;
   if ((r = cuda_check(launch_level_solve(D.tn_dev, D.ntens, 0, prm, st), "level solve"))) return r;
   int k = 5;
-  nblk = proj_nblk(1 << (dl - k));
+  nblk = proj_nblk(1 << (dl - k), nsh);
   if ((r = cuda_check(launch_project(true, D.sh_dev, nsh, k, nblk, 1, st), "project"))) return r;
   if ((r = reduce_grams(D, comm, nblk, st))) return r;
   int src_is_a = 1;
   ++k;
   while ((1ll << (dl - k + 1)) >= 256 && (1ll << (d - k + 1)) > FIN_COLS_HOST) {
     if ((r = cuda_check(launch_step_solve(D.tn_dev, D.ntens, k, 0, prm, st), "step solve"))) return r;
-    nblk = proj_nblk(1 << (dl - k));
+    nblk = proj_nblk(1 << (dl - k), nsh);
     if ((r = cuda_check(launch_project(false, D.sh_dev, nsh, k, nblk, src_is_a, st), "project"))) return r;
     if ((r = reduce_grams(D, comm, nblk, st))) return r;
     src_is_a ^= 1;
@@ -550,7 +550,7 @@ qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, c
   int prev_nb = 0;   // the Gram of step k is the reduced one in gsum
   while ((1ll << (d - k + 1)) > FIN_COLS_HOST) {
     if ((r = cuda_check(launch_step_solve(D.tn_dev, D.ntens, k, prev_nb, prm, st), "step solve"))) return r;
-    const int nb2 = proj_nblk(1 << (d - k));
+    const int nb2 = proj_nblk(1 << (d - k), D.ntens);
     if ((r = cuda_check(launch_project(false, D.tn_dev, D.ntens, k, nb2, src_is_a, st), "project"))) return r;
     src_is_a ^= 1;
     prev_nb = nb2;

@@ -51,8 +51,8 @@ cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams p
 // holds ntens * nlocal shard descriptors (tensor-major), `tn` ntens tensor
 // descriptors; shards of a tensor share its cores / ranks / proj / tau2 /
 // gsum.  nblk == 0 in a solve step means "read the reduced Gram gsum".
-int dec_nblk_loc(int dl);                                   // CTAs of the level-1 Gram pass
-int proj_nblk(int ncols);                                   // CTAs of a projection pass
+int dec_nblk_loc(int dl, int nprob);                        // CTAs per problem, level-1 Gram pass
+int proj_nblk(int ncols, int nprob);                        // CTAs per problem, projection pass
 static constexpr int FIN_COLS_HOST = 256;                   // finisher: W columns it holds
 cudaError_t launch_level_gram(const DecProb* sh, int nsh, int nblk, int* status, cudaStream_t st);
 cudaError_t launch_gram_reduce(const DecProb* sh, int ntens, int nlocal, int nblk, cudaStream_t st);

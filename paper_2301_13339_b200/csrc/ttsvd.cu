@@ -576,15 +576,21 @@ __global__ void __launch_bounds__(NT) k_gather_w(const DecProb* sh, const DecPro
   }
 }
 
-int dec_nblk_loc(int dl) {
-  uint64_t nchunks = 1ull << (dl - 12);
-  return (int)(nchunks < (uint64_t)NBLK_MAX ? nchunks : (uint64_t)NBLK_MAX);
+// CTAs per problem of a full-array pass: the whole launch targets
+// GRID_TARGET CTAs (4 per SM) however many problems it carries, so batched
+// launches keep several chunks per CTA (the cp.async double buffer reaches
+// steady state) and write few per-CTA partial Grams (8 KiB each).
+static constexpr int GRID_TARGET = 4 * 148;
+static inline int per_problem(uint64_t nchunks, int nprob) {
+  uint64_t want = (uint64_t)((GRID_TARGET + nprob - 1) / nprob);
+  if (want > (uint64_t)NBLK_MAX) want = NBLK_MAX;
+  if (want > nchunks) want = nchunks;
+  return want < 1 ? 1 : (int)want;
 }
 
-int proj_nblk(int ncols) {
-  int nc = ncols / 128;
-  return nc < NBLK_MAX ? nc : NBLK_MAX;
-}
+int dec_nblk_loc(int dl, int nprob) { return per_problem(1ull << (dl - 12), nprob); }
+
+int proj_nblk(int ncols, int nprob) { return per_problem((uint64_t)(ncols / 128), nprob); }
 
 cudaError_t launch_level_gram(const DecProb* sh, int nsh, int nblk, int* status, cudaStream_t st) {
   k_level_gram<<<dim3(nblk, nsh), NT, smem_level_gram(), st>>>(sh, nblk, status);
@@ -636,10 +642,9 @@ cudaError_t launch_gather_w(const DecProb* sh, const DecProb* tn, int ntens, int
 
 // ------------------------------------------------------------ host driver
 
-int dec_nblk(int d) {
+int dec_nblk(int d, int nprob) {
   if (d <= FIN_D) return 0;
-  uint64_t nchunks = 1ull << (d - 12);
-  return (int)(nchunks < (uint64_t)NBLK_MAX ? nchunks : (uint64_t)NBLK_MAX);
+  return dec_nblk_loc(d, nprob);
 }
 
 cudaError_t setup_ttsvd_kernels() {
@@ -666,15 +671,14 @@ cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams p
   if (d <= FIN_D) {
     return launch_finish(probs_dev, nprob, 1, 1, prm, st);
   }
-  const int nblk = dec_nblk(d);
+  const int nblk = dec_nblk(d, nprob);
   k_level_gram<<<dim3(nblk, nprob), NT, smem_level_gram(), st>>>(probs_dev, nblk, prm.status);
   count_launches(1);
   launch_level_solve(probs_dev, nprob, nblk, prm, st);
   // K3: W_m from x, Gram for step m+1
   int k = LVL_M;
   {
-    uint64_t nch = (1ull << (d - k)) / 128;
-    int nb = (int)(nch < (uint64_t)NBLK_MAX ? nch : (uint64_t)NBLK_MAX);
+    int nb = proj_nblk(1 << (d - k), nprob);
     k_project<true><<<dim3(nb, nprob), NT, smem_project(), st>>>(probs_dev, k, nb, 1);
     count_launches(1);
     int src_is_a = 1;  // W_m lives in Wa
@@ -683,8 +687,7 @@ cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams p
     // steps while W_{k-1} has more than FIN_COLS columns
     while ((1 << (d - k + 1)) > FIN_COLS) {
       launch_step_solve(probs_dev, nprob, k, prev_nb, prm, st);
-      uint64_t nc = (1ull << (d - k)) / 128;
-      int nb2 = (int)(nc < (uint64_t)NBLK_MAX ? nc : (uint64_t)NBLK_MAX);
+      int nb2 = proj_nblk(1 << (d - k), nprob);
       k_project<false><<<dim3(nb2, nprob), NT, smem_project(), st>>>(probs_dev, k, nb2, src_is_a);
       count_launches(1);
       src_is_a ^= 1;
