@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-fft-comparator", action="store_true")
     return ap.parse_args()
 
 
@@ -203,6 +204,34 @@ def chain_flops(d, rhat):
             "hadamard_round": (d - 1) * (36 * m ** 3 + 8 * (m * 64 * 64 + m * m * 64))}
 
 
+# ------------------------------------------------------------ cuFFT comparator
+def fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, steps, dev):
+    """y = scale * ifft(fft(f) fft(roll(g, -shift))) by cuFFT (D2Z / Z2D), the
+    dense method the paper compares against; returns its timing and the
+    relative L2 distance of the QTT result (y_d, already computed) to it."""
+    n1 = 1 << p["b"]
+    shape = (batch,) + (n1,) * D
+    f = f_d.view(shape)
+    g = g_d.view((n1,) * D)
+    dims = tuple(range(1, D + 1))
+    gs = torch.roll(g, shifts=tuple(-s for s in p["shift"][::-1]), dims=tuple(range(D)))
+    Gh = torch.fft.rfftn(gs, dim=tuple(range(D)))
+    out = torch.empty(shape, dtype=torch.float64, device=dev)
+
+    def conv():
+        out.copy_(torch.fft.irfftn(torch.fft.rfftn(f, dim=dims) * Gh, s=(n1,) * D, dim=dims) * p["scale"])
+
+    for _ in range(3):
+        conv()
+    torch.cuda.synchronize(dev)
+    ms = timed(conv, steps)
+    diff = float(torch.linalg.vector_norm(y_d.view(shape) - out) / torch.linalg.vector_norm(out))
+    el = batch * n1 ** D
+    return {"impl": "cuFFT (torch.fft rfftn/irfftn, float64)", "ms_per_step": ms / steps,
+            "value": el * steps / (ms / 1e3), "unit": "elements/s",
+            "rel_l2_qtt_vs_fft": diff}
+
+
 # ------------------------------------------------------------------- ours
 def run_ours(a):
     import torch
@@ -311,6 +340,12 @@ def run_ours(a):
         for k, v in Q.qtt_profile_read().items():
             stages[k] = stages.get(k, 0.0) + v / npf
     Q.qtt_profile_enable(False)
+    # dense comparator (paper Tables 2/4 last column): the same
+    # periodic convolution of the same noisy inputs by cuFFT (torch.fft) on this
+    # GPU, inputs resident, L2 flushed, same timing; not part of the metric
+    fftc = None
+    if mode != "sharded" and not a.no_fft_comparator:
+        fftc = fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, a.steps, dev)
 
     if world > 1:
         t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)
@@ -381,6 +416,9 @@ def run_ours(a):
         "ranks": {"f": rep["ranks_f"], "g": rep["ranks_g"], "out": rep["ranks_out"]},
         "status_bits": rep["status_bits"],
     }
+    if fftc is not None:
+        fftc["qtt_over_fft_time"] = (ms / a.steps) / fftc["ms_per_step"]
+        line["fft_comparator"] = fftc
     if not a.no_cpu_baseline and world == 1:
         if d <= 24:
             line["cpu_baseline"] = oracle_run(cfg, eps, a.cpu_seconds)
