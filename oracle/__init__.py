@@ -26,13 +26,14 @@ Parity status:
                                           Example 1.
 """
 
-from .qtt import (axes_descriptor, to_qtt, from_qtt, rank_rule, tt_svd, full,
-                  element, storage_count, ranks_of)
+from .qtt import (axes_descriptor, to_qtt, from_qtt, rank_rule, rank_rule_dropoff, choose_rank,
+                  tt_svd, full, element, storage_count, ranks_of)
 from .qfft import qfft, qifft, center, hadamard, round_full, round_local
 from .conv import conv_pipeline
 
 __all__ = [
-    "axes_descriptor", "to_qtt", "from_qtt", "rank_rule", "tt_svd", "full",
+    "axes_descriptor", "to_qtt", "from_qtt", "rank_rule", "rank_rule_dropoff", "choose_rank",
+    "tt_svd", "full",
     "element", "storage_count", "ranks_of", "qfft", "qifft", "center",
     "hadamard", "round_full", "round_local", "conv_pipeline",
 ]

@@ -18,7 +18,9 @@ def conv_pipeline(f, g, layout, dec, fft, shift, scale, return_info=False):
 
     f, g: float64 arrays, 1D (n,) or 2D (n, n) row-major with x fastest.
     layout: '1d' | 'interleaved' | 'concat'.
-    dec, fft: (eps, rmax, cluster_tol) for the TT-SVD and for QFFT/round/QiFFT.
+    dec, fft: (eps, rmax, cluster_tol) for the TT-SVD and for QFFT/round/QiFFT,
+    or (eps, rmax, cluster_tol, delta) for the SV drop-off rule (3) with the
+    same delta in both (eps unused, rmax = capacity cap).
     shift: per-axis integer shift (tuple, x first); scale: h = dx^D (Q12).
     """
     f = np.asarray(f, dtype=np.float64)

@@ -13,7 +13,7 @@ Q28 in DESIGN.md §3.
 
 import numpy as np
 
-from .qtt import rank_rule
+from .qtt import choose_rank
 
 
 def _twiddle(frac):
@@ -21,7 +21,7 @@ def _twiddle(frac):
     return np.exp(-2j * np.pi * frac)
 
 
-def round_local(C, p, eps, rmax, cluster_tol):
+def round_local(C, p, eps, rmax, cluster_tol, delta=None):
     """ROUND_LOCAL(p) (readings Q19/Q21/Q28).
 
     (i)  q = d..p+1: LQ of the r_{q-1} x 2 r_q unfolding of core q;
@@ -31,7 +31,8 @@ def round_local(C, p, eps, rmax, cluster_tol):
          r = RANK(sigma^2, tau^2, R, delta_c), core_c <- U_r,
          core_{c+1} <- (Sigma_r V_r^H) core_{c+1}.
     C is a list of complex cores (r_{k-1}, 2, r_k), modified in place;
-    p is 1-based.
+    p is 1-based.  `delta`: drop-off rule (3) instead of RANK (P:372-375:
+    the same delta as the TT-SVD).
     """
     d = len(C)
     for q in range(d, p, -1):
@@ -51,14 +52,14 @@ def round_local(C, p, eps, rmax, cluster_tol):
         r0, _, r1 = core.shape
         A = np.reshape(core, (2 * r0, r1), order="F")
         U, s, Vh = np.linalg.svd(A, full_matrices=False)
-        r = rank_rule(s * s, tau2, rmax, cluster_tol)
+        r = choose_rank(s * s, tau2, rmax, cluster_tol, delta)
         C[c - 1] = np.reshape(U[:, :r], (r0, 2, r), order="F")
         SV = s[:r, None] * Vh[:r, :]
         C[c] = np.einsum("ab,bcd->acd", SV, C[c])
     return C
 
 
-def qfft(cores, axes, bits, eps, rmax, cluster_tol=1e-10, stages=None):
+def qfft(cores, axes, bits, eps, rmax, cluster_tol=1e-10, delta=None, stages=None):
     """Unnormalised per-axis DFT (omega = e^{-2 pi i / 2^{b_a}})
     of a QTT tensor, truncated after every stage.
 
@@ -122,7 +123,7 @@ def qfft(cores, axes, bits, eps, rmax, cluster_tol=1e-10, stages=None):
             n[:r0, be, :] = c[:, be, :]
             n[r0:, be, :] = phi(d, be) * c[:, be, :]
         C[d - 1] = n
-        round_local(C, p, eps, rmax, cluster_tol)
+        round_local(C, p, eps, rmax, cluster_tol, delta)
         done += 1
     if stages is not None:
         return C
@@ -160,17 +161,17 @@ def hadamard(F, G):
     return Z
 
 
-def round_full(Z, eps, rmax, cluster_tol=1e-10):
+def round_full(Z, eps, rmax, cluster_tol=1e-10, delta=None):
     """TT-rounding ROUND_FULL = ROUND_LOCAL(1) (reading Q20/Q21, O5)."""
     C = [np.array(c, dtype=np.complex128) for c in Z]
-    return round_local(C, 1, eps, rmax, cluster_tol)
+    return round_local(C, 1, eps, rmax, cluster_tol, delta)
 
 
-def qifft(C, axes, bits, eps, rmax, cluster_tol=1e-10):
+def qifft(C, axes, bits, eps, rmax, cluster_tol=1e-10, delta=None):
     """QTT-iFFT (IDFT P:118-125): conj, qfft, conj, scale core_1
     by 2^{-d} = 1/N^D (reading Q23, O6)."""
     d = len(C)
-    out = qfft([np.conj(c) for c in C], axes, bits, eps, rmax, cluster_tol)
+    out = qfft([np.conj(c) for c in C], axes, bits, eps, rmax, cluster_tol, delta)
     out = [np.conj(c) for c in out]
     out[0] = out[0] * (2.0 ** (-d))
     return out

@@ -122,18 +122,64 @@ def rank_rule(lam, tau2, rmax, cluster_tol):
     return r
 
 
+def rank_rule_dropoff(lam, delta, rmax, cluster_tol):
+    """SV drop-off rule, modification (3): "if sigma_{k+1} /
+    sigma_k < delta ... truncate the singular values less than sigma_k", i.e.
+    keep sigma_1..sigma_k for the FIRST k (from the top) with a relative drop;
+    on lam = sigma^2 the test is lam_{k+1} < delta^2 lam_k.
+
+    Readings (N3): without a drop above it, values below the
+    floor sigma_k < 1e-7 sigma_1 (lam_k < 1e-14 lam_1) are discarded (the
+    paper is silent; SPEC S:149 floors at 1e-14 sigma_1, which only an SVD of
+    the unfolding resolves, not its Gram); the kernel capacity cap r <= R is
+    applied last and, when it cuts inside a cluster (Q6'), the cut moves
+    down to the cluster start as in RANK.
+    """
+    lam = np.maximum(np.asarray(lam, dtype=np.float64), 0.0)
+    m = lam.shape[0]
+    if m == 0 or not lam[0] > 0.0:
+        return 1
+    floor = 0
+    for k in range(m):
+        if lam[k] >= 1e-14 * lam[0]:
+            floor = k + 1
+    r_d = floor
+    for k in range(1, m):
+        if lam[k] < delta * delta * lam[k - 1]:
+            r_d = min(k, floor)
+            break
+    r = min(r_d, rmax)
+
+    def cl(q):
+        return q < m and lam[q - 1] > 0.0 and \
+            (lam[q - 1] - lam[q]) <= cluster_tol * lam[q - 1]
+
+    if r < r_d:
+        while r > 1 and cl(r):
+            r -= 1
+    return max(r, 1)
+
+
+def choose_rank(lam, tau2, rmax, cluster_tol, delta=None):
+    """RANK (modifications (1)) or, with delta given, the drop-off rule (3)."""
+    if delta is None:
+        return rank_rule(lam, tau2, rmax, cluster_tol)
+    return rank_rule_dropoff(lam, delta, rmax, cluster_tol)
+
+
 # ---------------------------------------------------------------------------
 # Alg. 1 TT-SVD with modification (1) (P:275-293, P:357-358)
 # ---------------------------------------------------------------------------
 
-def tt_svd(v, eps, rmax, cluster_tol=1e-10, return_info=False):
+def tt_svd(v, eps, rmax, cluster_tol=1e-10, delta=None, return_info=False):
     """Max-rank TT-SVD of a 2x...x2 tensor given as its QTT-ordered vector.
 
     tau = eps ||A||_F / sqrt(d-1) (P:282 with M-1 read as d-1, reading Q1).
     Step k: A^{k} = reshape(A, [2 r_{k-1}, |A|/(2 r_{k-1})]) (column-major,
     P:234/P:248), truncated SVD with ||E||_F <= tau and r_k <= R_max,
     core_k = reshape(U, [r_{k-1}, 2, r_k]), A := Sigma V^* (P:285-288);
-    core_d := A (P:290).
+    core_d := A.  With `delta` the truncation is modification (3)
+    (SV drop-off, rank_rule_dropoff) instead of eps / R_max.
     """
     v = np.asarray(v, dtype=np.float64).reshape(-1)
     n = v.shape[0]
@@ -150,7 +196,7 @@ def tt_svd(v, eps, rmax, cluster_tol=1e-10, return_info=False):
         M = np.reshape(W, (2 * r_prev, -1), order="F")
         shapes.append(M.shape)
         U, s, Vt = np.linalg.svd(M, full_matrices=False)
-        r = rank_rule(s * s, tau2, rmax, cluster_tol)
+        r = choose_rank(s * s, tau2, rmax, cluster_tol, delta)
         cores.append(np.reshape(U[:, :r], (r_prev, 2, r), order="F"))
         W = s[:r, None] * Vt[:r, :]
         r_prev = r
