@@ -73,11 +73,21 @@ typedef struct {
 } qtt_shape;
 
 /* Truncation policy: eps >= 0, 1 <= rmax <= 16, cluster_tol >= 0.
- * Decomposition caps use rmax (R_max); transform/rounding caps Rhat. */
+ * Decomposition caps use rmax (R_max); transform/rounding caps Rhat.
+ * rule = QTT_RULE_EPS (0): r = RANK(eps, rmax, cluster_tol) — modification
+ *   (1), tau^2 = eps^2 ||A||^2 / (d-1);
+ * rule = QTT_RULE_DROPOFF (1): SV drop-off, modification (3), P:363-365:
+ *   keep sigma_1..sigma_k at the first k with sigma_{k+1}/sigma_k < delta
+ *   (0 < delta < 1; no drop: keep sigma_k >= 1e-7 sigma_1), then the
+ *   capacity cap rmax (a cap inside a cluster moves down); eps unused.
+ *   The paper uses the same delta for the TT-SVD and the QTT-FFT. */
+enum { QTT_RULE_EPS = 0, QTT_RULE_DROPOFF = 1 };
 typedef struct {
   double eps;
   int rmax;
   double cluster_tol;
+  int rule;
+  double delta;
 } qtt_trunc;
 
 typedef struct qtt_tt_s* qtt_tt_t;      /* opaque TT tensor (batch of them)  */

@@ -138,6 +138,10 @@ qtt_status check_trunc(const qtt_trunc* t, int rmax_cap, const char* which) {
   if (t->rmax < 1 || t->rmax > rmax_cap)
     return fail(QTT_EINVAL, "%s rmax = %d outside [1, %d]", which, t->rmax, rmax_cap);
   if (!(t->cluster_tol >= 0.0)) return fail(QTT_EINVAL, "%s cluster_tol must be >= 0", which);
+  if (t->rule != QTT_RULE_EPS && t->rule != QTT_RULE_DROPOFF)
+    return fail(QTT_EINVAL, "%s rule = %d is not QTT_RULE_EPS / QTT_RULE_DROPOFF", which, t->rule);
+  if (t->rule == QTT_RULE_DROPOFF && !(t->delta > 0.0 && t->delta < 1.0))
+    return fail(QTT_EINVAL, "%s drop-off delta must lie in (0, 1)", which);
   return QTT_OK;
 }
 
@@ -227,7 +231,7 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
   if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), n * sizeof(DecProb), cudaMemcpyHostToDevice, st),
                       "copy descriptors")))
     return r;
-  DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status};
+  DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status, dec->rule, dec->delta};
   return cuda_check(launch_ttsvd(dp, n, d, prm, st), "TT-SVD launch");
 }
 
@@ -244,6 +248,8 @@ qtt_status run_transform(const std::vector<XfProb>& hv, const qtt_shape* s, cons
   P.eps = fft->eps;
   P.rmax = fft->rmax;
   P.ctol = fft->cluster_tol;
+  P.rule = fft->rule;
+  P.delta = fft->delta;
   P.inverse = inverse;
   P.scale = inverse ? scale * ldexp(1.0, -P.d) : 1.0;
   P.shift[0] = shift ? shift[0] : 0;
@@ -323,7 +329,7 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.do_center = 0;
   }
   if (cv.base) {
-    HrParams H{d, fft->eps, fft->rmax, fft->cluster_tol, status};
+    HrParams H{d, fft->eps, fft->rmax, fft->cluster_tol, status, fft->rule, fft->delta};
     if ((r = cuda_check(cudaMemcpyAsync(hp, hr.data(), nf * sizeof(HrProb), cudaMemcpyHostToDevice, st),
                         "copy descriptors")))
       return r;
@@ -713,7 +719,7 @@ qtt_status qtt_decompose(const double* x, const qtt_shape* shape, const qtt_trun
     Carver cv(ws);
     plan(cv, status, tt, D);
     if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
-    DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status};
+    DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status, dec->rule, dec->delta};
     if ((r = run_sharded_dec(D, comm, prm, st))) return r;
     *out = new_handle(shape, 1, dec->rmax, tt, status, st);
     return *out ? QTT_OK : fail(QTT_ENOMEM, "host allocation failed");
@@ -868,7 +874,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   TTAlloc F = take_tt(cv, nf, d), G = take_tt(cv, ng, d), Y = take_tt(cv, nf, d);
   if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
   prof_mark(0, st);
-  DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status};
+  DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status, dec->rule, dec->delta};
   if (comm) {
     // Step 1-2 column-sharded: f and g shards in one sequence, one allreduce per level
     const double* xs[2] = {f, g};

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     eig_values<2 * RH, NT>(S.E, rows);
     if (tid == 0) {
       int mp = rows < S.rb[c] ? rows : S.rb[c];
-      S.rk = rank_rule(S.E.lam, mp, S.tau2, P.rmax, P.ctol);
+      S.rk = rank_choose(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta);
     }
     __syncthreads();
     const int rk = S.rk;

@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       XT_MARK(2)
       if (tid == 0) {
         int mp = rows < S.rb[c] ? rows : S.rb[c];
-        S.rk = rank_rule(S.E.lam, mp, S.tau2, P.rmax, P.ctol);
+        S.rk = rank_choose(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta);
       }
       __syncthreads();
       const int rk = S.rk;

@@ -1087,4 +1087,39 @@ __device__ __forceinline__ int rank_rule(const double* lam, int m, double tau2, 
   return r;
 }
 
+// SV drop-off rule (modification (3); oracle rank_rule_dropoff):
+// first k with lam_{k+1} < delta^2 lam_k, no drop: lam_k >= 1e-14 lam_1;
+// then the cap, moved down out of a cluster when it binds.
+__device__ __forceinline__ int rank_rule_dropoff(const double* lam, int m, double delta, int rmax, double ctol) {
+  if (m <= 0) return 1;
+  const double l0 = fmax(lam[0], 0.0);
+  if (!(l0 > 0.0)) return 1;
+  int floor_ = 0;
+  for (int k = 0; k < m; ++k)
+    if (fmax(lam[k], 0.0) >= 1e-14 * l0) floor_ = k + 1;
+  int rd = floor_;
+  const double d2 = delta * delta;
+  for (int k = 1; k < m; ++k) {
+    if (fmax(lam[k], 0.0) < d2 * fmax(lam[k - 1], 0.0)) {
+      rd = k < floor_ ? k : floor_;
+      break;
+    }
+  }
+  int r = rd < rmax ? rd : rmax;
+  auto cl = [&](int q) -> bool {
+    if (q >= m) return false;
+    double a = fmax(lam[q - 1], 0.0), b = fmax(lam[q], 0.0);
+    return a > 0.0 && (a - b) <= ctol * a;
+  };
+  if (r < rd)
+    while (r > 1 && cl(r)) --r;
+  return r < 1 ? 1 : r;
+}
+
+// rank of a cut under the policy (rule 0: RANK, 1: drop-off)
+__device__ __forceinline__ int rank_choose(const double* lam, int m, double tau2, int rmax, double ctol, int rule,
+                                           double delta) {
+  return rule == 1 ? rank_rule_dropoff(lam, m, delta, rmax, ctol) : rank_rule(lam, m, tau2, rmax, ctol);
+}
+
 }  // namespace qtt

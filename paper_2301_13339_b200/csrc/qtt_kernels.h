@@ -42,6 +42,8 @@ struct DecParams {
   int rmax;
   double ctol;
   int* status;
+  int rule;          // 0: RANK (eps / rmax), 1: SV drop-off (delta)
+  double delta;
 };
 cudaError_t setup_ttsvd_kernels();
 cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st);
@@ -91,6 +93,8 @@ struct XfParams {
   double scale;      // multiplies core 1 of the output
   long long shift[2];
   int* status;
+  int rule;
+  double delta;
 };
 static constexpr int GR_XF = 4 * RS_XF * RS_XF;   // complex per GR slot
 cudaError_t setup_xf_kernels();
@@ -112,6 +116,8 @@ struct HrParams {
   int rmax;
   double ctol;
   int* status;
+  int rule;
+  double delta;
 };
 static constexpr int GR_HR = 64 * 64;
 cudaError_t setup_hr_kernels();

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nb
     eig_values<NE, NT>(S.E, rr);
     if (tid == 0) {
       int mp = rr < (1 << (d - k)) ? rr : (1 << (d - k));
-      S.rk = rank_rule(S.E.lam, mp, tau2, prm.rmax, prm.ctol);
+      S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
     }
     __syncthreads();
     const int rk = S.rk;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
   eig_values<NE, NT>(S.E, rr);
   if (tid == 0) {
     int mp = rr < (1 << (pr.d - k)) ? rr : (1 << (pr.d - k));
-    S.rk = rank_rule(S.E.lam, mp, *pr.tau2, prm.rmax, prm.ctol);
+    S.rk = rank_choose(S.E.lam, mp, *pr.tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
   }
   __syncthreads();
   const int rk = S.rk;
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart,
     eig_values<NE, NT>(S.E, rr);
     if (tid == 0) {
       int mp = rr < n ? rr : n;
-      S.rk = rank_rule(S.E.lam, mp, tau2, prm.rmax, prm.ctol);
+      S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
     }
     __syncthreads();
     const int rk = S.rk;

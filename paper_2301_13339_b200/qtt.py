@@ -33,7 +33,8 @@ class Shape(ctypes.Structure):
 
 
 class Trunc(ctypes.Structure):
-    _fields_ = [("eps", ctypes.c_double), ("rmax", ctypes.c_int), ("cluster_tol", ctypes.c_double)]
+    _fields_ = [("eps", ctypes.c_double), ("rmax", ctypes.c_int), ("cluster_tol", ctypes.c_double),
+                ("rule", ctypes.c_int), ("delta", ctypes.c_double)]
 
 
 class Report(ctypes.Structure):
@@ -126,8 +127,12 @@ def shape(D, bits, layout="1d", batch=1, f_stride=0, g_stride=0, y_stride=0):
     return Shape(D, b, LAYOUTS[layout], batch, f_stride, g_stride, y_stride)
 
 
-def trunc(eps, rmax, cluster_tol=1e-10):
-    return Trunc(eps, rmax, cluster_tol)
+def trunc(eps, rmax, cluster_tol=1e-10, delta=None):
+    """Truncation policy: RANK(eps, rmax, cluster_tol) (modification (1)), or
+    with `delta` the SV drop-off rule (modification (3)) capped at rmax."""
+    if delta is None:
+        return Trunc(eps, rmax, cluster_tol, 0, 0.0)
+    return Trunc(eps, rmax, cluster_tol, 1, float(delta))
 
 
 def _shift(shift):

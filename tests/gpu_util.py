@@ -42,6 +42,17 @@ def gpu_decompose(x, layout, eps, rmax, ctol=1e-10):
     return tt
 
 
+def gpu_decompose_policy(x, layout, dec):
+    """TT-SVD on the GPU with a full truncation tuple (eps, rmax, ctol[, delta])."""
+    xd = dev(x)
+    shp = shape_of(x, layout)
+    D = Q.trunc(*dec)
+    fft = Q.trunc(dec[0], min(dec[1], 8), dec[2])
+    nb = Q.qtt_workspace_bytes(shp, D, fft)
+    w = ws(nb)
+    return Q.qtt_decompose(xd.data_ptr(), shp, D, w.data_ptr(), nb, stream(), ws_owner=(w, xd))
+
+
 def gpu_full(tt, like, imag=False):
     """Expand a TT handle to a full array shaped like `like` (complex if imag)."""
     n = like.size

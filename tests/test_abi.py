@@ -83,3 +83,13 @@ def test_invalid_arguments_fail_before_any_device_work(L):
                          ctypes.byref(Q.trunc(1e-3, 8)), None, 1.0, ctypes.c_void_p(256), 1024,
                          None, None, None)
     assert st == Q.QTT_ENOMEM
+
+
+def test_truncation_rule_validation(L):
+    shp = Q.shape(2, [9, 9], "interleaved")
+    fft = Q.trunc(1e-3, 8)
+    ok = Q.trunc(0.0, 10, 1e-10, delta=0.02)
+    assert ok.rule == 1 and ok.delta == 0.02
+    assert L.qtt_workspace_bytes(ctypes.byref(shp), ctypes.byref(ok), ctypes.byref(fft), 1) > 0
+    for bad in (Q.Trunc(0.0, 10, 1e-10, 1, 0.0), Q.Trunc(0.0, 10, 1e-10, 1, 1.0), Q.Trunc(1e-3, 10, 1e-10, 7, 0.1)):
+        assert L.qtt_workspace_bytes(ctypes.byref(shp), ctypes.byref(bad), ctypes.byref(fft), 1) == 0
