@@ -20,6 +20,12 @@ Parity status:
                                           exact reconstruction, Lemma 1).
   * qfft / qifft / center / hadamard   — pinned (numpy.fft, closed-form DFTs,
                                           Parseval, per-stage invariant).
+  * rank_rule_dropoff (modification 3) — pinned (rule cases, exact low rank,
+                                          Table 1 I_delta, Example 2 exact).
+  * rng.omega / qtt.rsvd_step          — pinned (N(0,1) statistics,
+    (modification 2, TT-RSVD)            exactness on low rank, Eq.
+                                          rsvd_error bound, fallback rule,
+                                          Table 1 I_QTT_r).
   * round_full / conv_pipeline         — pinned at eps=0 by brute-force
                                           periodic convolution; with caps by
                                           the paper's Table 1 E2 band for
@@ -30,6 +36,7 @@ from .qtt import (axes_descriptor, to_qtt, from_qtt, rank_rule, rank_rule_dropof
                   tt_svd, full, element, storage_count, ranks_of)
 from .qfft import qfft, qifft, center, hadamard, round_full, round_local
 from .conv import conv_pipeline
+from . import rng
 
 __all__ = [
     "axes_descriptor", "to_qtt", "from_qtt", "rank_rule", "rank_rule_dropoff", "choose_rank",

@@ -9,7 +9,7 @@ from .qtt import axes_descriptor, to_qtt, from_qtt, tt_svd, full
 from .qfft import qfft, qifft, center, hadamard, round_full
 
 
-def conv_pipeline(f, g, layout, dec, fft, shift, scale, return_info=False):
+def conv_pipeline(f, g, layout, dec, fft, shift, scale, return_info=False, rsvd=None):
     """y_j = scale * sum_i f_i g_{(j - i + shift) mod n} per axis, computed as
     Alg. 2: Step 1 reshape to 2x..x2, Step 2 max-rank TT-SVD of
     both (Alg. 1 + mod (1)), Step 3 QiFFT(QFFT(F) (.) QFFT(G))
@@ -32,8 +32,10 @@ def conv_pipeline(f, g, layout, dec, fft, shift, scale, return_info=False):
     lay = "1d" if D == 1 else layout
     vf = to_qtt(f, lay)
     vg = to_qtt(g, lay)
-    F = tt_svd(vf, *dec)
-    G = tt_svd(vg, *dec)
+    # rsvd = (p, seed_f, seed_g): max-rank TT-RSVD (modification (2)) for the
+    # TT-SVD of f and g (reading N2: the QTT-FFT / rounding keep (1))
+    F = tt_svd(vf, *dec, rsvd=None if rsvd is None else (rsvd[0], rsvd[1]))
+    G = tt_svd(vg, *dec, rsvd=None if rsvd is None else (rsvd[0], rsvd[2]))
     Fh = qfft(F, axes, bits, *fft)
     Gh = qfft(G, axes, bits, *fft)
     Gh = center(Gh, axes, bits, shift)

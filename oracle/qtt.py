@@ -171,7 +171,22 @@ def choose_rank(lam, tau2, rmax, cluster_tol, delta=None):
 # Alg. 1 TT-SVD with modification (1)
 # ---------------------------------------------------------------------------
 
-def tt_svd(v, eps, rmax, cluster_tol=1e-10, delta=None, return_info=False):
+def rsvd_step(A, k, p, seed, step):
+    """Randomized SVD of Appendix A (Alg. "Solving the Fixed-Rank
+    Problem" + Alg. "RSVD", [HMT11] Alg. 5.1): Omega (n x (k+p)) ~ N(0,1)
+    (oracle.rng, counter = TT-SVD step), Y = A Omega, Q R = Y, B = Q^* A,
+    U~ Sigma V^* = B, U = Q U~.  Returns (U, s, Vh) like numpy.linalg.svd."""
+    from .rng import omega
+    n = A.shape[1]
+    Om = omega(seed, step, np.arange(n), k + p)
+    Y = A @ Om
+    Q, _ = np.linalg.qr(Y)
+    B = Q.conj().T @ A
+    Ut, s, Vh = np.linalg.svd(B, full_matrices=False)
+    return Q @ Ut, s, Vh
+
+
+def tt_svd(v, eps, rmax, cluster_tol=1e-10, delta=None, return_info=False, rsvd=None):
     """Max-rank TT-SVD of a 2x...x2 tensor given as its QTT-ordered vector.
 
     tau = eps ||A||_F / sqrt(d-1) (P:282 with M-1 read as d-1, reading Q1).
@@ -179,7 +194,10 @@ def tt_svd(v, eps, rmax, cluster_tol=1e-10, delta=None, return_info=False):
     P:234/P:248), truncated SVD with ||E||_F <= tau and r_k <= R_max,
     core_k = reshape(U, [r_{k-1}, 2, r_k]), A := Sigma V^* (P:285-288);
     core_d := A.  With `delta` the truncation is modification (3)
-    (SV drop-off, rank_rule_dropoff) instead of eps / R_max.
+    (SV drop-off, rank_rule_dropoff) instead of eps / R_max.  With
+    rsvd = (p, seed) the SVD of step k is the randomized SVD with k = R_max
+    and oversampling p (modification (2)), except when
+    min(m_k, n_k) <= R_max + p, where it reverts to the SVD.
     """
     v = np.asarray(v, dtype=np.float64).reshape(-1)
     n = v.shape[0]
@@ -195,7 +213,10 @@ def tt_svd(v, eps, rmax, cluster_tol=1e-10, delta=None, return_info=False):
     for k in range(1, d):
         M = np.reshape(W, (2 * r_prev, -1), order="F")
         shapes.append(M.shape)
-        U, s, Vt = np.linalg.svd(M, full_matrices=False)
+        if rsvd is not None and min(M.shape) > rmax + rsvd[0]:
+            U, s, Vt = rsvd_step(M, rmax, rsvd[0], rsvd[1], k)
+        else:
+            U, s, Vt = np.linalg.svd(M, full_matrices=False)
         r = choose_rank(s * s, tau2, rmax, cluster_tol, delta)
         cores.append(np.reshape(U[:, :r], (r_prev, 2, r), order="F"))
         W = s[:r, None] * Vt[:r, :]
