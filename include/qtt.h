@@ -81,13 +81,23 @@ typedef struct {
  *   (0 < delta < 1; no drop: keep sigma_k >= 1e-7 sigma_1), then the
  *   capacity cap rmax (a cap inside a cluster moves down); eps unused.
  *   The paper uses the same delta for the TT-SVD and the QTT-FFT. */
-enum { QTT_RULE_EPS = 0, QTT_RULE_DROPOFF = 1 };
+enum { QTT_RULE_EPS = 0, QTT_RULE_DROPOFF = 1, QTT_RULE_RSVD = 2 };
+/* rule = QTT_RULE_RSVD (2), decomposition only: RANK as rule 0, but every
+ *   TT-SVD step whose unfolding has min(m, n) > rmax + p uses the
+ *   randomized SVD of Appendix A (modification (2)):
+ *   Y = A Omega with Omega (n x (rmax + p)) ~ N(0,1) from the counter-based
+ *   generator of DESIGN.md §3 (key seed + t for tensor t of a call: the f
+ *   batch entries 0..B-1, then g), range(Y) -> Rayleigh-Ritz.  Requires
+ *   8 <= rmax + p <= 16 and no communicator.  The QTT-FFT / rounding keep
+ *   rule 0 or 1 (reading N2). */
 typedef struct {
   double eps;
   int rmax;
   double cluster_tol;
   int rule;
   double delta;
+  int p;                     /* TT-RSVD oversampling */
+  unsigned long long seed;   /* TT-RSVD generator key */
 } qtt_trunc;
 
 typedef struct qtt_tt_s* qtt_tt_t;      /* opaque TT tensor (batch of them)  */
@@ -216,6 +226,12 @@ qtt_status qtt_shard_geometry(const qtt_shape* shape, int nshards, int shard,
  * Stream-ordered. */
 int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, int mode,
                    void* stream);
+
+/* TEST-ONLY: rows j0 .. j0+n-1 of the TT-RSVD test matrix Omega_k (step k,
+ * key seed) as a row-major n x kp device array, so tests can compare the
+ * generator with the oracle's (oracle/rng.py).  Stream-ordered. */
+int qtt_debug_omega(unsigned long long seed, int k, unsigned long long j0, int n, int kp, double* out,
+                    void* stream);
 
 /* TEST-ONLY: build a handle from host cores (shape->batch tensors; tensor i,
  * core k occupies the slot of 512 complex starting at ((i*d)+k)*512, compact

@@ -132,14 +132,16 @@ qtt_status check_shape(const qtt_shape* s) {
   return QTT_OK;
 }
 
-qtt_status check_trunc(const qtt_trunc* t, int rmax_cap, const char* which) {
+qtt_status check_trunc(const qtt_trunc* t, int rmax_cap, const char* which, bool allow_rsvd = false) {
   if (!t) return fail(QTT_EINVAL, "%s truncation is NULL", which);
   if (!(t->eps >= 0.0)) return fail(QTT_EINVAL, "%s eps must be >= 0", which);
   if (t->rmax < 1 || t->rmax > rmax_cap)
     return fail(QTT_EINVAL, "%s rmax = %d outside [1, %d]", which, t->rmax, rmax_cap);
   if (!(t->cluster_tol >= 0.0)) return fail(QTT_EINVAL, "%s cluster_tol must be >= 0", which);
-  if (t->rule != QTT_RULE_EPS && t->rule != QTT_RULE_DROPOFF)
-    return fail(QTT_EINVAL, "%s rule = %d is not QTT_RULE_EPS / QTT_RULE_DROPOFF", which, t->rule);
+  if (t->rule != QTT_RULE_EPS && t->rule != QTT_RULE_DROPOFF && !(allow_rsvd && t->rule == QTT_RULE_RSVD))
+    return fail(QTT_EINVAL, "%s rule = %d is not allowed here", which, t->rule);
+  if (t->rule == QTT_RULE_RSVD && !(t->p >= 0 && t->rmax + t->p >= 8 && t->rmax + t->p <= 16))
+    return fail(QTT_EINVAL, "%s TT-RSVD needs p >= 0 and 8 <= rmax + p <= 16", which);
   if (t->rule == QTT_RULE_DROPOFF && !(t->delta > 0.0 && t->delta < 1.0))
     return fail(QTT_EINVAL, "%s drop-off delta must lie in (0, 1)", which);
   return QTT_OK;
@@ -160,6 +162,18 @@ void axes_of(const qtt_shape* s, int* axis, int* bit) {
   }
 }
 
+DecParams dec_params(const qtt_trunc* dec, int* status) {
+  DecParams prm{};
+  prm.eps = dec->eps;
+  prm.rmax = dec->rmax;
+  prm.ctol = dec->cluster_tol;
+  prm.status = status;
+  prm.rule = dec->rule == QTT_RULE_RSVD ? QTT_RULE_EPS : dec->rule;
+  prm.delta = dec->delta;
+  prm.kp = dec->rule == QTT_RULE_RSVD ? dec->rmax + dec->p : 0;
+  return prm;
+}
+
 struct TTAlloc {
   cplx* cores;
   int* ranks;
@@ -177,13 +191,15 @@ struct DecScratch {
   double* part;
   double* proj;
   double* tau2;
+  double* psk;
 };
-DecScratch take_dec(Carver& cv, int d) {
+DecScratch take_dec(Carver& cv, int d, bool rsvd = false) {
   DecScratch s{};
   if (d > 12) {
     s.Wa = cv.take<double>((size_t)RC << (d - 5));
     s.Wb = cv.take<double>((size_t)RC << (d - 6));
     s.part = cv.take<double>((size_t)NBLK_MAX * 1024);
+    if (rsvd) s.psk = cv.take<double>((size_t)NBLK_MAX * 1024);
   } else {
     s.Wa = s.Wb = s.part = nullptr;
   }
@@ -212,8 +228,9 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
                          const qtt_trunc* dec, TTAlloc tt, Carver& cv, int* status, cudaStream_t st) {
   const int d = shape_d(s);
   std::vector<DecProb> h(n);
+  const bool rsvd = dec->rule == QTT_RULE_RSVD;
   for (int i = 0; i < n; ++i) {
-    DecScratch sc = take_dec(cv, d);
+    DecScratch sc = take_dec(cv, d, rsvd);
     DecProb& p = h[i];
     p.x = base + (size_t)i * (size_t)stride;
     p.layout = s->layout;
@@ -224,6 +241,8 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
     p.Wa = sc.Wa; p.Wb = sc.Wb; p.part = sc.part; p.proj = sc.proj; p.tau2 = sc.tau2;
     p.cores = tt.cores + (size_t)i * d * SLOT;
     p.ranks = tt.ranks + (size_t)i * 64;
+    p.psk = sc.psk;
+    p.seed = dec->seed + (unsigned long long)i;
   }
   DecProb* dp = cv.take<DecProb>(n);
   if (!cv.base) return QTT_OK;
@@ -231,7 +250,7 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
   if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), n * sizeof(DecProb), cudaMemcpyHostToDevice, st),
                       "copy descriptors")))
     return r;
-  DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status, dec->rule, dec->delta};
+  DecParams prm = dec_params(dec, status);
   return cuda_check(launch_ttsvd(dp, n, d, prm, st), "TT-SVD launch");
 }
 
@@ -667,8 +686,9 @@ const char* qtt_build_info(void) {
 }
 
 size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const qtt_trunc* fft, int nranks) {
-  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec") || check_trunc(fft, RH_MAX, "fft") || nranks < 1)
+  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec", true) || check_trunc(fft, RH_MAX, "fft") || nranks < 1)
     return 0;
+  if (nranks > 1 && dec->rule == QTT_RULE_RSVD) return 0;
   if (nranks > 1) return ws_sharded(shape, fft, nranks, 1);
   const int d = shape_d(shape);
   const int nf = shape->batch, ng = shape->g_stride == 0 ? 1 : shape->batch;
@@ -677,7 +697,7 @@ size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const q
   TTAlloc F = take_tt(cv, nf, d), G = take_tt(cv, ng, d), Y = take_tt(cv, nf, d);
   // decomposition scratch and descriptors, then Step 3 and Step 4 scratch
   // (dry runs of the same carving sequence qtt_conv_full performs)
-  for (int i = 0; i < nf + ng; ++i) take_dec(cv, d);
+  for (int i = 0; i < nf + ng; ++i) take_dec(cv, d, dec->rule == QTT_RULE_RSVD);
   cv.take<DecProb>(nf + ng);
   run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, nullptr, 1.0, Y, cv, nullptr, nullptr);
   run_expand(Y.cores, Y.ranks, nf, d, nullptr, 0, shape, 0, cv, nullptr);
@@ -697,7 +717,7 @@ qtt_status qtt_decompose(const double* x, const qtt_shape* shape, const qtt_trun
   qtt_status r;
   if ((r = check_shape(shape))) return r;
   if (!x || !out) return fail(QTT_EINVAL, "x / out is NULL");
-  if ((r = check_trunc(dec, comm ? RS_GATHER : RC, "dec"))) return r;
+  if ((r = check_trunc(dec, comm ? RS_GATHER : RC, "dec", !comm))) return r;
   cudaError_t ce;
   if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
   const int d = shape_d(shape);
@@ -719,7 +739,7 @@ qtt_status qtt_decompose(const double* x, const qtt_shape* shape, const qtt_trun
     Carver cv(ws);
     plan(cv, status, tt, D);
     if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
-    DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status, dec->rule, dec->delta};
+    DecParams prm = dec_params(dec, status);
     if ((r = run_sharded_dec(D, comm, prm, st))) return r;
     *out = new_handle(shape, 1, dec->rmax, tt, status, st);
     return *out ? QTT_OK : fail(QTT_ENOMEM, "host allocation failed");
@@ -845,7 +865,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
                          void* stream, qtt_comm_t comm, qtt_report* rep_host) {
   qtt_status r;
   if ((r = check_shape(shape))) return r;
-  if ((r = check_trunc(dec, RS_XF, "dec"))) return r;
+  if ((r = check_trunc(dec, RS_XF, "dec", !comm))) return r;
   if ((r = check_trunc(fft, RH_MAX, "fft"))) return r;
   if (!f || !g || !y) return fail(QTT_EINVAL, "f / g / y is NULL");
   ShardGeom geo{};
@@ -874,7 +894,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   TTAlloc F = take_tt(cv, nf, d), G = take_tt(cv, ng, d), Y = take_tt(cv, nf, d);
   if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
   prof_mark(0, st);
-  DecParams prm{dec->eps, dec->rmax, dec->cluster_tol, status, dec->rule, dec->delta};
+  DecParams prm = dec_params(dec, status);
   if (comm) {
     // Step 1-2 column-sharded: f and g shards in one sequence, one allreduce per level
     const double* xs[2] = {f, g};
@@ -889,7 +909,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
     for (int i = 0; i < nf + ng; ++i) {
       const bool isf = i < nf;
       const int j = isf ? i : i - nf;
-      DecScratch sc = take_dec(cv, d_);
+      DecScratch sc = take_dec(cv, d_, dec->rule == QTT_RULE_RSVD);
       DecProb& p = h[i];
       p.x = isf ? f + (size_t)j * (size_t)fs : g + (size_t)j * (size_t)gs;
       p.layout = shape->layout;
@@ -900,6 +920,8 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
       p.Wa = sc.Wa; p.Wb = sc.Wb; p.part = sc.part; p.proj = sc.proj; p.tau2 = sc.tau2;
       p.cores = (isf ? F.cores : G.cores) + (size_t)j * d_ * SLOT;
       p.ranks = (isf ? F.ranks : G.ranks) + (size_t)j * 64;
+      p.psk = sc.psk;
+      p.seed = dec->seed + (unsigned long long)i;   // f batch entries, then g
     }
     DecProb* dp = cv.take<DecProb>(nf + ng);
     if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), h.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),

@@ -31,7 +31,26 @@ __global__ void __launch_bounds__(NT) k_debug_eigh(const cplx* A, int n, double*
     for (int k = 0; k < 5; ++k) sweeps[7 + k] = (int)E.u.tr.tstep[k];
   }
 }
+__global__ void k_debug_omega(unsigned long long seed, int k, unsigned long long j0, int n, int kp, double* out) {
+  const int npairs = (kp + 1) / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * npairs; e += gridDim.x * blockDim.x) {
+    const int row = e / npairs, cp = e % npairs;
+    double z0, z1;
+    omega_pair(j0 + row, (unsigned)k, (unsigned)cp, seed, z0, z1);
+    out[(size_t)row * kp + 2 * cp] = z0;
+    if (2 * cp + 1 < kp) out[(size_t)row * kp + 2 * cp + 1] = z1;
+  }
+}
 }  // namespace qtt
+
+extern "C" int qtt_debug_omega(unsigned long long seed, int k, unsigned long long j0, int n, int kp, double* out,
+                               void* stream) {
+  using namespace qtt;
+  if (n < 1 || kp < 1 || kp > 64 || !out) return QTT_EINVAL;
+  k_debug_omega<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(seed, k, j0, n, kp, out);
+  count_launches(1);
+  return cudaGetLastError() == cudaSuccess ? QTT_OK : QTT_ECUDA;
+}
 
 extern "C" int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* sweeps, int reps, int mode,
                               void* stream) {

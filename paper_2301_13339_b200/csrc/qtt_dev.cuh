@@ -1087,6 +1087,37 @@ __device__ __forceinline__ int rank_rule(const double* lam, int m, double tau2, 
   return r;
 }
 
+// ------------------------------------------------------ TT-RSVD generator
+// Omega_k[j, c] of the randomized SVD (modification (2); Appendix
+// A "Omega_ij ~ N(0,1)"), the counter-based generator defined in
+// DESIGN.md §3 (reading N2-rng) and implemented independently by
+// oracle/rng.py: ten Philox-4x32 rounds on counter (j lo, j hi, k, c >> 1)
+// with key (seed lo, seed hi), two 53-bit uniforms, Box-Muller pair; value
+// z_{c mod 2}.
+__device__ __forceinline__ void omega_pair(unsigned long long j, unsigned k, unsigned cp, unsigned long long seed,
+                                           double& z0, double& z1) {
+  unsigned c0 = (unsigned)j, c1 = (unsigned)(j >> 32), c2 = k, c3 = cp;
+  unsigned k0 = (unsigned)seed, k1 = (unsigned)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const unsigned hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    c0 = hi1 ^ c1 ^ k0;
+    c1 = lo1;
+    c2 = hi0 ^ c3 ^ k1;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const double u1 = ((double)(c0 >> 5) * 67108864.0 + (double)(c1 >> 6) + 0.5) * (1.0 / 9007199254740992.0);
+  const double u2 = ((double)(c2 >> 5) * 67108864.0 + (double)(c3 >> 6) + 0.5) * (1.0 / 9007199254740992.0);
+  const double rad = sqrt(-2.0 * log(u1));
+  double sn, cs;
+  sincospi(2.0 * u2, &sn, &cs);
+  z0 = rad * cs;
+  z1 = rad * sn;
+}
+
 // SV drop-off rule (modification (3); oracle rank_rule_dropoff):
 // first k with lam_{k+1} < delta^2 lam_k, no drop: lam_k >= 1e-14 lam_1;
 // then the cap, moved down out of a cluster when it binds.

@@ -36,14 +36,17 @@ struct DecProb {
   double* tau2;      // per-cut threshold tau^2
   cplx* cores;       // d slots
   int* ranks;        // r_0..r_d
+  double* psk;       // per-CTA partial sketches Y = A Omega [NBLK_MAX][32*32] (TT-RSVD)
+  unsigned long long seed;   // Omega key of this tensor (TT-RSVD)
 };
 struct DecParams {
   double eps;
   int rmax;
   double ctol;
   int* status;
-  int rule;          // 0: RANK (eps / rmax), 1: SV drop-off (delta)
+  int rule;          // 0: RANK (eps / rmax), 1: SV drop-off (delta), 2: RANK + TT-RSVD
   double delta;
+  int kp;            // TT-RSVD sketch width k + p = rmax + p (0: plain SVD steps)
 };
 cudaError_t setup_ttsvd_kernels();
 cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st);
@@ -58,8 +61,10 @@ int proj_nblk(int ncols, int nprob);                        // CTAs per problem,
 static constexpr int FIN_COLS_HOST = 256;                   // finisher: W columns it holds
 cudaError_t launch_level_gram(const DecProb* sh, int nsh, int nblk, int* status, cudaStream_t st);
 cudaError_t launch_gram_reduce(const DecProb* sh, int ntens, int nlocal, int nblk, cudaStream_t st);
-cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st);
-cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st);
+// nsk: number of per-CTA partial TT-RSVD sketches to sum (0 = none)
+cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st, int nsk = 0);
+cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st,
+                              int nsk = 0);
 cudaError_t launch_project(bool from_x, const DecProb* pr, int nprob, int k, int nblk, int src_is_a,
                            cudaStream_t st);
 cudaError_t launch_finish(const DecProb* tn, int ntens, int k, int src_is_a, DecParams prm, cudaStream_t st);

@@ -28,7 +28,10 @@ static constexpr int CH = 4096;                 // chunk elements (64 x 64 squar
 static constexpr int CH_COLS = CH / LVL_ROWS;   // 128 columns of X_m per chunk
 static constexpr int SLD = 68;                  // smem row stride of an interleaved chunk
 static constexpr int S1D = 36;                  // smem stride of a 32-element column (1D)
-static constexpr int CHUNK_SMEM = 64 * SLD;     // doubles per chunk buffer (>= 128*36)
+// doubles per chunk buffer: the larger of the interleaved 64 x 64 tile (ld
+// SLD) and the 1D / concat 128 columns of 32 (ld S1D)
+static constexpr int CHUNK_SMEM = (64 * SLD > 128 * S1D) ? 64 * SLD : 128 * S1D;
+static_assert(CHUNK_SMEM >= 31 + S1D * 127 + 1 && CHUNK_SMEM >= 63 + SLD * 63 + 1, "chunk buffer too small");
 
 // ------------------------------------------------------------ chunk I/O
 // chunk-local QTT index -> smem offset
@@ -162,6 +165,247 @@ __global__ void __launch_bounds__(NT) k_level_gram(const DecProb* probs, int nbl
   gram_reduce_cta(acc, smem, out);
 }
 
+// ------------------------------------------------------ TT-RSVD sketches
+// Modification (2) (Appendix A): Y_k = A^{k} Omega_k,
+// Omega_k[j, c] from omega_pair(j, k, c >> 1, seed) (j = column of A^{k}).
+// Partial sketches per CTA go to psk[blk * 1024 + i + 32 c].
+static constexpr int KPMAX = 16;
+static constexpr int OLD = KPMAX + 1;     // smem ld of an Omega tile row
+
+struct SketchXSmem {
+  double tile[CHUNK_SMEM];
+  double om5[128 * OLD];                  // Omega_5 rows j = 128 c + col
+  double om4[256 * OLD];                  // Omega_4 rows b5 + 2 j
+  double red[8][1024];
+};
+
+// Level sketches from x (one extra pass): Z_5 = X_5 Omega_5 (32 x kp) and,
+// if need4, Z_4[a, c] = sum_{b5, j} X_5[a + 16 b5, j] Omega_4[b5 + 2 j, c]
+// (16 x kp), X_5 = reshape(x, [32, 2^{d-5}]).  Then Y_k = (I2 (x) P_{k-1})^T Z_k.
+__global__ void __launch_bounds__(NT) k_sketch_x(const DecProb* probs, int nblk, int kp, int need4) {
+  const DecProb& pr = probs[blockIdx.y];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  SketchXSmem& S = *reinterpret_cast<SketchXSmem*>(smraw);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const uint64_t nchunks = 1ull << (pr.dl - 12);
+  const int rb = lane >> 2, cb = lane & 3;                 // Z_5: rows 4rb.., cols 4cb..
+  const int rb4 = (lane >> 2) & 3, b5 = lane >> 4;         // Z_4: rows 4rb4.., half b5
+  double a5[4][4], a4[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) a5[i][q] = a4[i][q] = 0.0;
+  int ro5[4], ro4[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    ro5[i] = chunk_off(4 * rb + i, pr.layout);
+    ro4[i] = chunk_off(4 * rb4 + i + 16 * b5, pr.layout);
+  }
+  const int npairs = (kp + 1) / 2;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += nblk) {
+    load_chunk_async(S.tile, pr.x, c, pr.layout, pr.bx);
+    cp_async_commit();
+    for (int e = tid; e < (need4 ? 384 : 128) * npairs; e += NT) {
+      const int row = e / npairs, cp = e % npairs;
+      double z0, z1;
+      if (row < 128) {
+        omega_pair(c * 128 + row, 5u, (unsigned)cp, pr.seed, z0, z1);
+        S.om5[row * OLD + 2 * cp] = z0;
+        S.om5[row * OLD + 2 * cp + 1] = z1;
+      } else {
+        const int r4 = row - 128;
+        omega_pair(c * 256 + r4, 4u, (unsigned)cp, pr.seed, z0, z1);
+        S.om4[r4 * OLD + 2 * cp] = z0;
+        S.om4[r4 * OLD + 2 * cp + 1] = z1;
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int col = w; col < 128; col += NT / 32) {
+      const int coff = chunk_off((uint32_t)col << LVL_M, pr.layout);
+      double xv[4], ov[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xv[i] = S.tile[ro5[i] + coff];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) ov[q] = S.om5[col * OLD + 4 * cb + q];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a5[i][q] = fma(xv[i], ov[q], a5[i][q]);
+      if (need4) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xv[i] = S.tile[ro4[i] + coff];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ov[q] = S.om4[(b5 + 2 * col) * OLD + 4 * cb + q];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a4[i][q] = fma(xv[i], ov[q], a4[i][q]);
+      }
+    }
+    __syncthreads();
+  }
+  // fixed-order reduction over the 8 warps (and the two b5 halves of Z_4)
+  double* mine = S.red[w];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      mine[(4 * rb + i) + 32 * (4 * cb + q)] = a5[i][q];
+      mine[512 + (b5 ? 16 : 0) + (4 * rb4 + i) + 32 * (4 * cb + q)] = a4[i][q];
+    }
+  __syncthreads();
+  double* out = pr.psk + (size_t)blockIdx.x * 1024;
+  for (int e = tid; e < 1024; e += NT) {
+    double t = 0.0;
+#pragma unroll
+    for (int ww = 0; ww < NT / 32; ++ww) t += S.red[ww][e];
+    S.red[0][e] = t;   // safe: each e read by its own thread only
+  }
+  __syncthreads();
+  for (int e = tid; e < 1024; e += NT) {
+    if (e < 512) {
+      out[e] = S.red[0][e];
+    } else {
+      // Z_4 halves: rows i (< 16) at 512 + i + 32 c and 512 + 16 + i + 32 c
+      const int f = e - 512, i = f & 31, cc = f >> 5;
+      out[e] = (i < 16) ? S.red[0][512 + i + 32 * cc] + S.red[0][512 + 16 + i + 32 * cc] : 0.0;
+    }
+  }
+}
+
+struct SketchWSmem {
+  double A[32 * 64];                      // 64 columns of A^{k+1} (ld rr)
+  double om[64 * OLD];
+  double red[8][512];
+};
+
+// Sketch of A^{k+1} = reshape(W_k, [2 r_k, 2^{d-k-1}]) (column-major: A's
+// column j is W's columns 2j, 2j+1): Y_{k+1} = A^{k+1} Omega_{k+1} (rr x kp).
+__global__ void __launch_bounds__(NT) k_sketch_w(const DecProb* probs, int k, int nblk, int src_is_a, int kp) {
+  const DecProb& pr = probs[blockIdx.y];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  SketchWSmem& S = *reinterpret_cast<SketchWSmem*>(smraw);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int rr = 2 * pr.ranks[k];
+  const double* W = src_is_a ? pr.Wa : pr.Wb;
+  const uint64_t ncols = 1ull << (pr.dl - k - 1);
+  const uint64_t nchunks = (ncols + 63) / 64;
+  const int rb = lane >> 2, cb = lane & 3;
+  const int npairs = (kp + 1) / 2;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += nblk) {
+    const int nc = (int)((ncols - c * 64) < 64 ? (ncols - c * 64) : 64);
+    for (int e = tid; e < rr * nc; e += NT) S.A[e] = W[c * 64 * rr + e];
+    for (int e = tid; e < nc * npairs; e += NT) {
+      const int row = e / npairs, cp = e % npairs;
+      double z0, z1;
+      omega_pair(c * 64 + row, (unsigned)(k + 1), (unsigned)cp, pr.seed, z0, z1);
+      S.om[row * OLD + 2 * cp] = z0;
+      S.om[row * OLD + 2 * cp + 1] = z1;
+    }
+    __syncthreads();
+    if (4 * rb < rr) {
+      for (int j = w; j < nc; j += NT / 32) {
+        double av[4], ov[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = (4 * rb + i < rr) ? S.A[(4 * rb + i) + rr * j] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ov[q] = S.om[j * OLD + 4 * cb + q];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[i][q] = fma(av[i], ov[q], acc[i][q]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) S.red[w][(4 * rb + i) + 32 * (4 * cb + q)] = acc[i][q];
+  __syncthreads();
+  double* out = pr.psk + (size_t)blockIdx.x * 1024;
+  for (int e = tid; e < 1024; e += NT) {
+    double t = 0.0;
+    if (e < 512)
+#pragma unroll
+      for (int ww = 0; ww < NT / 32; ++ww) t += S.red[ww][e];
+    out[e] = t;
+  }
+}
+
+// RSVD truncation of one cut (Appendix A, in Gram form): G = A A^T
+// (rr x rr, row-major ld 32), Y = A Omega (rr x kp, Y[i + 32 c]).  Q = the kp
+// leading eigenvectors of Y Y^T (an orthonormal basis of range(Y), the Q of
+// "QR = Y"), B B^T = Q^T G Q (B = Q^* A), its eigenpairs give Sigma^2 and
+// U~, U = Q U~.  Writes U_r to UB[i + 32 r] and returns r = RANK(Sigma^2).
+struct RsvdBuf {
+  double GK[1024];
+  double QB[512];
+  double UB[512];
+  double TB[512];
+  double Y[512];
+  int rk;
+};
+
+template <int NE>
+__device__ int rsvd_truncate(EigSmem<NE>& E, RsvdBuf& R, int rr, int kp, double tau2, const DecParams& prm) {
+  constexpr int LD = EigSmem<NE>::LD;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < rr * rr; e += NT) {
+    const int i = e % rr, j = e / rr;
+    double t = 0.0;
+    for (int c = 0; c < kp; ++c) t = fma(R.Y[i + 32 * c], R.Y[j + 32 * c], t);
+    E.A[0][i + LD * j] = cmk(t, 0.0);
+  }
+  __syncthreads();
+  eig_values<NE, NT>(E, rr);
+  const cplx* Q = eig_vectors<NE, NT>(E, rr, kp, prm.status);
+  for (int e = tid; e < rr * kp; e += NT) {
+    const int i = e % rr, c = e / rr;
+    R.QB[i + 32 * c] = Q[i + LD * c].x;
+  }
+  __syncthreads();
+  // TB = G Q (rr x kp), then E.A = Q^T TB (kp x kp)
+  for (int e = tid; e < rr * kp; e += NT) {
+    const int i = e % rr, c = e / rr;
+    double t = 0.0;
+    for (int j = 0; j < rr; ++j) t = fma(R.GK[i * 32 + j], R.QB[j + 32 * c], t);
+    R.TB[i + 32 * c] = t;
+  }
+  __syncthreads();
+  for (int e = tid; e < kp * kp; e += NT) {
+    const int a = e % kp, b = e / kp;
+    double t = 0.0;
+    for (int i = 0; i < rr; ++i) t = fma(R.QB[i + 32 * a], R.TB[i + 32 * b], t);
+    E.A[0][a + LD * b] = cmk(t, 0.0);
+  }
+  __syncthreads();
+  eig_values<NE, NT>(E, kp);
+  if (tid == 0) R.rk = rank_choose(E.lam, kp, tau2, prm.rmax, prm.ctol, 0, 0.0);
+  __syncthreads();
+  const int rk = R.rk;
+  const cplx* Ut = eig_vectors<NE, NT>(E, kp, rk, prm.status);
+  for (int e = tid; e < rr * rk; e += NT) {
+    const int i = e % rr, r = e / rr;
+    double t = 0.0;
+    for (int a = 0; a < kp; ++a) t = fma(R.QB[i + 32 * a], Ut[a + LD * r].x, t);
+    R.UB[i + 32 * r] = t;
+  }
+  __syncthreads();
+  return rk;
+}
+
+// the TT-RSVD applies at step k when min(m_k, n_k) > R_max + p
+__device__ __forceinline__ bool use_rsvd(const DecParams& prm, int rr, uint64_t ncols) {
+  return prm.kp > 0 && rr > prm.kp && ncols > (uint64_t)prm.kp;
+}
+
 // ------------------------------------------------------------------- K2
 // shared helper: write U_r as core k (slot k-1) and ranks[k]
 __device__ void write_core_from_U(const DecProb& pr, int k, const cplx* U, int ld, int rr, int rk) {
@@ -173,6 +417,25 @@ __device__ void write_core_from_U(const DecProb& pr, int k, const cplx* U, int l
   if (threadIdx.x == 0) pr.ranks[k] = rk;
 }
 
+__device__ void write_core_from_Ud(const DecProb& pr, int k, const double* U, int rr, int rk) {
+  cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
+  for (int e = threadIdx.x; e < rr * rk; e += NT) {
+    int a = e % rr, r = e / rr;
+    core[a + rr * r] = cmk(U[a + 32 * r], 0.0);
+  }
+  if (threadIdx.x == 0) pr.ranks[k] = rk;
+}
+
+// sum of nsk per-CTA partial sketches (rows < rows_, kp columns) into R.Y
+__device__ void gather_sketch(const DecProb& pr, int nsk, int off, int rows_, int kp, double* Y) {
+  for (int e = threadIdx.x; e < rows_ * kp; e += NT) {
+    const int i = e % rows_, c = e / rows_;
+    double t = 0.0;
+    for (int b = 0; b < nsk; ++b) t += pr.psk[(size_t)b * 1024 + off + i + 32 * c];
+    Y[i + 32 * c] = t;
+  }
+}
+
 template <int NE>
 struct LevelSolveSmem {
   EigSmem<NE> E;
@@ -180,10 +443,11 @@ struct LevelSolveSmem {
   double P[2][32 * 16];
   double PT[1024];
   int rk;
+  RsvdBuf R;
 };
 
 template <int NE>
-__global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nblk, DecParams prm) {
+__global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nblk, DecParams prm, int nsk) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
   LevelSolveSmem<NE>& S = *reinterpret_cast<LevelSolveSmem<NE>*>(smraw);
@@ -228,24 +492,45 @@ __global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nb
         s += Pp[jl + 32 * rho] * t;
       }
       S.E.A[0][i + LD * j] = cmk(s, 0.0);
+      S.R.GK[i * 32 + j] = s;
     }
     __syncthreads();
-    eig_values<NE, NT>(S.E, rr);
-    if (tid == 0) {
-      int mp = rr < (1 << (d - k)) ? rr : (1 << (d - k));
-      S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
+    int rk;
+    const cplx* U = nullptr;
+    const bool rs = (k == 4 || k == 5) && nsk > 0 && use_rsvd(prm, rr, 1ull << (d - k));
+    if (rs) {
+      // Y_k = (I2 (x) P_{k-1})^T Z_k, Z_5 at psk offset 0 (32 rows), Z_4 at 512 (16 rows)
+      gather_sketch(pr, nsk, k == 5 ? 0 : 512, n2, prm.kp, S.R.TB);
+      __syncthreads();
+      for (int e = tid; e < rr * prm.kp; e += NT) {
+        const int i = e % rr, c = e / rr;
+        const int rho = i % r_prev, be = i / r_prev;
+        double t = 0.0;
+        for (int a = 0; a < h; ++a) t = fma(Pp[a + 32 * rho], S.R.TB[(a + h * be) + 32 * c], t);
+        S.R.Y[i + 32 * c] = t;
+      }
+      __syncthreads();
+      rk = rsvd_truncate<NE>(S.E, S.R, rr, prm.kp, tau2, prm);
+      write_core_from_Ud(pr, k, S.R.UB, rr, rk);
+    } else {
+      eig_values<NE, NT>(S.E, rr);
+      if (tid == 0) {
+        int mp = rr < (1 << (d - k)) ? rr : (1 << (d - k));
+        S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
+      }
+      __syncthreads();
+      rk = S.rk;
+      U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
+      write_core_from_U(pr, k, U, LD, rr, rk);
     }
-    __syncthreads();
-    const int rk = S.rk;
-    const cplx* U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
-    write_core_from_U(pr, k, U, LD, rr, rk);
     // P_k[a][r] = sum_rho P_{k-1}[a mod h][rho] U[rho + r_prev (a div h)][r]
     double* Pn = S.P[cur ^ 1];
     for (int e = tid; e < n2 * rk; e += NT) {
       int a = e % n2, r = e / n2;
       int al = a % h, ah = a / h;
       double s = 0.0;
-      for (int rho = 0; rho < r_prev; ++rho) s += Pp[al + 32 * rho] * U[rho + r_prev * ah + LD * r].x;
+      for (int rho = 0; rho < r_prev; ++rho)
+        s += Pp[al + 32 * rho] * (rs ? S.R.UB[rho + r_prev * ah + 32 * r] : U[rho + r_prev * ah + LD * r].x);
       Pn[a + 32 * r] = s;
     }
     __syncthreads();
@@ -382,10 +667,11 @@ template <int NE>
 struct StepSolveSmem {
   EigSmem<NE> E;
   int rk;
+  RsvdBuf R;
 };
 
 template <int NE>
-__global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, int nblk, DecParams prm) {
+__global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, int nblk, DecParams prm, int nsk) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
   StepSolveSmem<NE>& S = *reinterpret_cast<StepSolveSmem<NE>*>(smraw);
@@ -398,8 +684,20 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
     if (nblk == 0) s = pr.gsum[i * 32 + j];   // Gram already reduced (across shards)
     for (int b = 0; b < nblk; ++b) s += pr.part[(size_t)b * 1024 + i * 32 + j];
     S.E.A[0][i + LD * j] = cmk(s, 0.0);
+    S.R.GK[i * 32 + j] = s;
   }
   __syncthreads();
+  if (nsk > 0 && use_rsvd(prm, rr, 1ull << (pr.d - k))) {
+    gather_sketch(pr, nsk, 0, rr, prm.kp, S.R.Y);
+    __syncthreads();
+    const int rk = rsvd_truncate<NE>(S.E, S.R, rr, prm.kp, *pr.tau2, prm);
+    write_core_from_Ud(pr, k, S.R.UB, rr, rk);
+    for (int e = tid; e < rr * rk; e += NT) {
+      int a = e % rr, r = e / rr;
+      pr.proj[a + 32 * r] = S.R.UB[a + 32 * r];
+    }
+    return;
+  }
   eig_values<NE, NT>(S.E, rr);
   if (tid == 0) {
     int mp = rr < (1 << (pr.d - k)) ? rr : (1 << (pr.d - k));
@@ -423,6 +721,7 @@ static constexpr int FIN_D = 12;                  // d <= 12: whole TT-SVD in on
 template <int NE>
 struct FinishSmem {
   double B[2][FIN_CAP];
+  RsvdBuf R;
   EigSmem<NE> E;
   double G[1024];
   int rk;
@@ -494,24 +793,57 @@ __global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart,
     for (int e = tid; e < rr * rr; e += NT) {
       int i = e % rr, j = e / rr;
       S.E.A[0][i + LD * j] = cmk(S.G[i * 32 + j], 0.0);
+      S.R.GK[i * 32 + j] = S.G[i * 32 + j];
     }
     __syncthreads();
-    eig_values<NE, NT>(S.E, rr);
-    if (tid == 0) {
-      int mp = rr < n ? rr : n;
-      S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
+    int rk;
+    const cplx* U = nullptr;
+    const bool rs = use_rsvd(prm, rr, (uint64_t)n);
+    if (rs) {
+      // Y = A Omega_k directly from the unfolding in smem (A = B[cur], rr x n),
+      // Omega generated in blocks of 64 rows into the free buffer
+      double* om = S.B[cur ^ 1];
+      const int npairs = (prm.kp + 1) / 2;
+      for (int e = tid; e < rr * prm.kp; e += NT) S.R.Y[(e % rr) + 32 * (e / rr)] = 0.0;
+      for (int j0 = 0; j0 < n; j0 += 64) {
+        const int nb = n - j0 < 64 ? n - j0 : 64;
+        for (int e = tid; e < nb * npairs; e += NT) {
+          const int row = e / npairs, cp = e % npairs;
+          double z0, z1;
+          omega_pair((unsigned long long)(j0 + row), (unsigned)k, (unsigned)cp, pr.seed, z0, z1);
+          om[row * OLD + 2 * cp] = z0;
+          om[row * OLD + 2 * cp + 1] = z1;
+        }
+        __syncthreads();
+        for (int e = tid; e < rr * prm.kp; e += NT) {
+          const int i = e % rr, c = e / rr;
+          double t = 0.0;
+          for (int j = 0; j < nb; ++j) t = fma(S.B[cur][i + rr * (j0 + j)], om[j * OLD + c], t);
+          S.R.Y[i + 32 * c] += t;
+        }
+        __syncthreads();
+      }
+      rk = rsvd_truncate<NE>(S.E, S.R, rr, prm.kp, tau2, prm);
+      write_core_from_Ud(pr, k, S.R.UB, rr, rk);
+    } else {
+      eig_values<NE, NT>(S.E, rr);
+      if (tid == 0) {
+        int mp = rr < n ? rr : n;
+        S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
+      }
+      __syncthreads();
+      rk = S.rk;
+      U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
+      write_core_from_U(pr, k, U, LD, rr, rk);
     }
-    __syncthreads();
-    const int rk = S.rk;
-    const cplx* U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
-    write_core_from_U(pr, k, U, LD, rr, rk);
     // W_k = U_r^T M_k
     const double* M = S.B[cur];
     double* Wn = S.B[cur ^ 1];
+    __syncthreads();
     for (int e = tid; e < rk * n; e += NT) {
       int r = e % rk, j = e / rk;
       double s = 0.0;
-      for (int a = 0; a < rr; ++a) s += U[a + LD * r].x * M[a + rr * j];
+      for (int a = 0; a < rr; ++a) s += (rs ? S.R.UB[a + 32 * r] : U[a + LD * r].x) * M[a + rr * j];
       Wn[r + rk * j] = s;
     }
     __syncthreads();
@@ -604,16 +936,17 @@ cudaError_t launch_gram_reduce(const DecProb* sh, int ntens, int nlocal, int nbl
   return cudaGetLastError();
 }
 
-cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st) {
-  if (narrow(prm)) k_level_solve<20><<<dim3(1, ntens), NT, smem_level_solve<20>(), st>>>(tn, nblk, prm);
-  else k_level_solve<32><<<dim3(1, ntens), NT, smem_level_solve<32>(), st>>>(tn, nblk, prm);
+cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st, int nsk) {
+  if (narrow(prm)) k_level_solve<20><<<dim3(1, ntens), NT, smem_level_solve<20>(), st>>>(tn, nblk, prm, nsk);
+  else k_level_solve<32><<<dim3(1, ntens), NT, smem_level_solve<32>(), st>>>(tn, nblk, prm, nsk);
   count_launches(1);
   return cudaGetLastError();
 }
 
-cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st) {
-  if (narrow(prm)) k_step_solve<20><<<dim3(1, ntens), NT, smem_step_solve<20>(), st>>>(tn, k, nblk, prm);
-  else k_step_solve<32><<<dim3(1, ntens), NT, smem_step_solve<32>(), st>>>(tn, k, nblk, prm);
+cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st,
+                              int nsk) {
+  if (narrow(prm)) k_step_solve<20><<<dim3(1, ntens), NT, smem_step_solve<20>(), st>>>(tn, k, nblk, prm, nsk);
+  else k_step_solve<32><<<dim3(1, ntens), NT, smem_step_solve<32>(), st>>>(tn, k, nblk, prm, nsk);
   count_launches(1);
   return cudaGetLastError();
 }
@@ -662,6 +995,8 @@ cudaError_t setup_ttsvd_kernels() {
   QTT_SET_SMEM(k_step_solve<32>, smem_step_solve<32>())
   QTT_SET_SMEM(k_finish<20>, smem_finish<20>())
   QTT_SET_SMEM(k_finish<32>, smem_finish<32>())
+  QTT_SET_SMEM(k_sketch_x, sizeof(SketchXSmem))
+  QTT_SET_SMEM(k_sketch_w, sizeof(SketchWSmem))
 #undef QTT_SET_SMEM
   return cudaSuccess;
 }
@@ -674,7 +1009,15 @@ cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams p
   const int nblk = dec_nblk(d, nprob);
   k_level_gram<<<dim3(nblk, nprob), NT, smem_level_gram(), st>>>(probs_dev, nblk, prm.status);
   count_launches(1);
-  launch_level_solve(probs_dev, nprob, nblk, prm, st);
+  // TT-RSVD (modification (2)): level sketches Z_5 (and Z_4) from one more pass over x
+  int nsx = 0;
+  if (prm.kp > 0 && (1ull << (d - LVL_M)) > (uint64_t)prm.kp) {
+    nsx = nblk;
+    const int need4 = (16 > prm.kp) && ((1ull << (d - 4)) > (uint64_t)prm.kp);
+    k_sketch_x<<<dim3(nsx, nprob), NT, sizeof(SketchXSmem), st>>>(probs_dev, nsx, prm.kp, need4);
+    count_launches(1);
+  }
+  launch_level_solve(probs_dev, nprob, nblk, prm, st, nsx);
   // K3: W_m from x, Gram for step m+1
   int k = LVL_M;
   {
@@ -686,7 +1029,14 @@ cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams p
     ++k;
     // steps while W_{k-1} has more than FIN_COLS columns
     while ((1 << (d - k + 1)) > FIN_COLS) {
-      launch_step_solve(probs_dev, nprob, k, prev_nb, prm, st);
+      // TT-RSVD: sketch of A^{k} = reshape(W_{k-1}) when its columns exceed k + p
+      int nsk = 0;
+      if (prm.kp > 0 && (1ull << (d - k)) > (uint64_t)prm.kp) {
+        nsk = per_problem((1ull << (d - k)) / 64, nprob);
+        k_sketch_w<<<dim3(nsk, nprob), NT, sizeof(SketchWSmem), st>>>(probs_dev, k - 1, nsk, src_is_a, prm.kp);
+        count_launches(1);
+      }
+      launch_step_solve(probs_dev, nprob, k, prev_nb, prm, st, nsk);
       int nb2 = proj_nblk(1 << (d - k), nprob);
       k_project<false><<<dim3(nb2, nprob), NT, smem_project(), st>>>(probs_dev, k, nb2, src_is_a);
       count_launches(1);

@@ -11,7 +11,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqtt.so")
+LIB_PATH = os.environ.get("QTT_LIB", os.path.join(HERE, "libqtt.so"))   # override: diagnostics builds
 
 QTT_OK, QTT_EINVAL, QTT_ENUMERIC, QTT_ECUDA, QTT_ENCCL, QTT_ENOMEM = range(6)
 LAYOUTS = {"1d": 0, "interleaved": 1, "concat": 2}
@@ -22,7 +22,7 @@ SYMBOLS = [
     "qtt_destroy", "qtt_status_string", "qtt_last_error", "qtt_build_info",
     "qtt_debug_eigh", "qtt_debug_tt_from_host", "qtt_profile_enable", "qtt_profile_read",
     "qtt_launch_count", "qtt_comm_workspace_bytes", "qtt_comm_unique_id", "qtt_comm_init",
-    "qtt_comm_init_virtual", "qtt_comm_destroy", "qtt_shard_geometry",
+    "qtt_comm_init_virtual", "qtt_comm_destroy", "qtt_shard_geometry", "qtt_debug_omega",
 ]
 
 
@@ -34,7 +34,8 @@ class Shape(ctypes.Structure):
 
 class Trunc(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("rmax", ctypes.c_int), ("cluster_tol", ctypes.c_double),
-                ("rule", ctypes.c_int), ("delta", ctypes.c_double)]
+                ("rule", ctypes.c_int), ("delta", ctypes.c_double), ("p", ctypes.c_int),
+                ("seed", ctypes.c_ulonglong)]
 
 
 class Report(ctypes.Structure):
@@ -110,6 +111,8 @@ def lib():
     L.qtt_comm_destroy.argtypes = [P]
     L.qtt_shard_geometry.restype = I
     L.qtt_shard_geometry.argtypes = [pS, I, I, pLL, ctypes.POINTER(ctypes.c_int)]
+    L.qtt_debug_omega.restype = I
+    L.qtt_debug_omega.argtypes = [ctypes.c_ulonglong, I, ctypes.c_ulonglong, I, I, P, P]
     L.qtt_debug_tt_from_host.restype = I
     L.qtt_debug_tt_from_host.argtypes = [pS, P, ctypes.POINTER(ctypes.c_int), I, P, S, P, pH]
     _LIB = L
@@ -127,12 +130,16 @@ def shape(D, bits, layout="1d", batch=1, f_stride=0, g_stride=0, y_stride=0):
     return Shape(D, b, LAYOUTS[layout], batch, f_stride, g_stride, y_stride)
 
 
-def trunc(eps, rmax, cluster_tol=1e-10, delta=None):
-    """Truncation policy: RANK(eps, rmax, cluster_tol) (modification (1)), or
-    with `delta` the SV drop-off rule (modification (3)) capped at rmax."""
+def trunc(eps, rmax, cluster_tol=1e-10, delta=None, rsvd=None):
+    """Truncation policy: RANK(eps, rmax, cluster_tol) (modification (1));
+    with `delta` the SV drop-off rule (modification (3)) capped at rmax; with
+    rsvd = (p, seed) the max-rank TT-RSVD (modification (2), decomposition
+    only)."""
+    if rsvd is not None:
+        return Trunc(eps, rmax, cluster_tol, 2, 0.0, int(rsvd[0]), int(rsvd[1]))
     if delta is None:
-        return Trunc(eps, rmax, cluster_tol, 0, 0.0)
-    return Trunc(eps, rmax, cluster_tol, 1, float(delta))
+        return Trunc(eps, rmax, cluster_tol, 0, 0.0, 0, 0)
+    return Trunc(eps, rmax, cluster_tol, 1, float(delta), 0, 0)
 
 
 def _shift(shift):
@@ -284,6 +291,11 @@ def qtt_debug_tt_from_host(shp, cores_c128, ranks_i32, rcap, ws_ptr, ws_bytes, s
                                         ranks_i32.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
                                         rcap, ws_ptr, ws_bytes, stream, ctypes.byref(h)))
     return TT(h, ws_owner)
+
+
+def qtt_debug_omega(seed, k, j0, n, kp, out_ptr, stream=0):
+    """Test-only: Omega_k rows j0..j0+n-1 (row-major n x kp) on the device."""
+    _check(lib().qtt_debug_omega(seed, k, j0, n, kp, out_ptr, stream))
 
 
 STAGES = ["ttsvd", "qfft", "hadamard_round", "qifft", "expand"]

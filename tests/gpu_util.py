@@ -43,7 +43,7 @@ def gpu_decompose(x, layout, eps, rmax, ctol=1e-10):
 
 
 def gpu_decompose_policy(x, layout, dec):
-    """TT-SVD on the GPU with a full truncation tuple (eps, rmax, ctol[, delta])."""
+    """TT-SVD on the GPU with a full truncation tuple (eps, rmax, ctol[, delta[, rsvd]])."""
     xd = dev(x)
     shp = shape_of(x, layout)
     D = Q.trunc(*dec)

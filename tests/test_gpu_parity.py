@@ -42,6 +42,9 @@ DEC_CASES = [
     ("2d_int_c2_kernel", lambda: synth.kernel(2, 9, 60.0), "interleaved", 1e-3, 10),
     ("1d_c1", lambda: synth.signal("c1"), "1d", 1e-3, 10),
     ("2d_int_d12_small", lambda: synth.random_signal((64, 64), 7, "smooth"), "interleaved", 1e-4, 8),
+    # several 4096-element chunks per CTA (double-buffered cp.async) in the 1D / concat layouts
+    ("1d_d22_multichunk", lambda: synth.random_signal((1 << 22,), 8, "smooth"), "1d", 1e-3, 10),   # T2 probe 1.9e-15
+    ("2d_cat_d22_multichunk", lambda: synth.random_signal((2048, 2048), 9, "smooth"), "concat", 1e-4, 10),
 ]
 
 
