@@ -419,6 +419,13 @@ def run_ours(a):
     if fftc is not None:
         fftc["qtt_over_fft_time"] = (ms / a.steps) / fftc["ms_per_step"]
         line["fft_comparator"] = fftc
+    # the small-core chain is a serial sequence of truncations (latency-bound):
+    # forward transforms (F and G concurrently), rounding, inverse transform
+    cuts = d * (d - 1) // 2
+    chain_ms = stages.get("qfft", 0.0) + stages.get("hadamard_round", 0.0) + stages.get("qifft", 0.0)
+    line["chain"] = {"sequential_truncations": 2 * cuts + (d - 1), "ms": round(chain_ms, 4),
+                     "us_per_truncation": round(1e3 * chain_ms / (2 * cuts + (d - 1)), 2),
+                     "share_of_step": round(chain_ms / (ms / a.steps), 4)}
     if not a.no_cpu_baseline and world == 1:
         if d <= 24:
             line["cpu_baseline"] = oracle_run(cfg, eps, a.cpu_seconds)
