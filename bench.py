@@ -136,7 +136,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -205,7 +205,7 @@ def chain_flops(d, rhat):
 
 
 # ------------------------------------------------------------ cuFFT comparator
-def fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, steps, dev):
+def fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, steps, dev, clean=None):
     """y = scale * ifft(fft(f) fft(roll(g, -shift))) by cuFFT (D2Z / Z2D), the
     dense method the paper compares against; returns its timing and the
     relative L2 distance of the QTT result (y_d, already computed) to it."""
@@ -227,9 +227,20 @@ def fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, steps, dev):
     ms = timed(conv, steps)
     diff = float(torch.linalg.vector_norm(y_d.view(shape) - out) / torch.linalg.vector_norm(out))
     el = batch * n1 ** D
-    return {"impl": "cuFFT (torch.fft rfftn/irfftn, float64)", "ms_per_step": ms / steps,
-            "value": el * steps / (ms / 1e3), "unit": "elements/s",
-            "rel_l2_qtt_vs_fft": diff}
+    res = {"impl": "cuFFT (torch.fft rfftn/irfftn, float64)", "ms_per_step": ms / steps,
+           "value": el * steps / (ms / 1e3), "unit": "elements/s",
+           "rel_l2_qtt_vs_fft": diff}
+    if clean is not None:
+        # the paper's quality metric E2 (Table 1): both results against
+        # the convolution of the CLEAN signal (batch entry 0)
+        c = torch.from_numpy(clean).to(dev).view((n1,) * D)
+        ref = torch.fft.irfftn(torch.fft.rfftn(c, dim=tuple(range(D))) * Gh, s=(n1,) * D,
+                               dim=tuple(range(D))) * p["scale"]
+        nr = torch.linalg.vector_norm(ref)
+        res["e2_vs_clean_conv"] = {
+            "qtt": float(torch.linalg.vector_norm(y_d.view(shape)[0] - ref) / nr),
+            "fft_of_noisy_data": float(torch.linalg.vector_norm(out[0] - ref) / nr)}
+    return res
 
 
 # ------------------------------------------------------------------- ours
@@ -345,7 +356,9 @@ def run_ours(a):
     # GPU, inputs resident, L2 flushed, same timing; not part of the metric
     fftc = None
     if mode != "sharded" and not a.no_fft_comparator:
-        fftc = fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, a.steps, dev)
+        clean0 = synth.signal(cfg, index=rank * batch if mode == "batch" else rank, noisy=False)
+        fftc = fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, a.steps, dev,
+                              clean=np.ascontiguousarray(clean0))
 
     if world > 1:
         t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)
