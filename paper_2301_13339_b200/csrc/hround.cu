@@ -12,7 +12,7 @@
 
 namespace qtt {
 
-static constexpr int NT = 256;
+static constexpr int NT = 512;   // one CTA per SM (190 KB smem): more warps to hide the product latencies
 static constexpr int RH = RH_MAX;       // 8
 static constexpr int RZ = RH * RH;      // 64
 static constexpr int CZ = 2 * RH * RH;  // compact core of F or G
@@ -127,6 +127,9 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     }
     __syncthreads();
   }
+#ifdef QTT_HR_GR_ONLY
+  return;   // timing experiment only: right Gram chain alone
+#endif
   // ---------------- LQ rank bounds
   if (tid == 0) {
     S.rb[d] = 1;

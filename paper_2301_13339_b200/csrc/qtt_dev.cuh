@@ -490,7 +490,8 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #endif
     // T is unitarily similar to A / ||A||_F: its spectrum lies in [-1, 1]
     double lo = -1.0 - 1e-14, hi = 1.0 + 1e-14;
-    const int gl = n <= 8 ? 32 : (n <= 16 ? 16 : 8);      // threads per eigenvalue
+    // threads per eigenvalue: the largest power of two <= 32 with n groups in NT
+    const int gl = (n * 32 <= NT) ? 32 : (n * 16 <= NT ? 16 : 8);
     const int k = tid / gl, j = tid % gl;
     const int steps = gl == 32 ? 11 : (gl == 16 ? 13 : 17);
     const double sj = (double)(j + 1) / (double)(gl + 1);
