@@ -388,15 +388,27 @@ def run_ours(a):
     dom = max(stages, key=stages.get) if stages else "ttsvd"
     bound, amount = alg[dom]
     dur = stages.get(dom, 0.0) / 1e3
+    # DRAM traffic of the dominant kernel from the committed ncu --set full
+    # capture (profiles/*_ncu_<kernel>.json), per launch; null without one
+    traffic = None
+    try:
+        import glob as _glob
+        caps = sorted(_glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json")))
+        for cp in caps:
+            cj = json.load(open(cp))
+            if cj.get("stage") == dom:
+                traffic = cj.get("dram_bytes_per_launch")
+    except Exception:
+        traffic = None
     if bound == "hbm":
         ach = amount / dur / 1e9 if dur else None
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm if ach else None, "traffic": None,
+                "frac": ach / hbm if ach else None, "traffic": traffic,
                 "kernel": dom, "peak_source": src}
     else:
         ach = amount / dur / 1e12 if dur else None
         roof = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_PEAK_TFLOPS if ach else None, "traffic": None,
+                "frac": ach / FP64_PEAK_TFLOPS if ach else None, "traffic": traffic,
                 "kernel": dom, "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
     passes = {}
     for k in ("ttsvd", "expand"):
