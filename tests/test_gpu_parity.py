@@ -195,3 +195,49 @@ def test_nonfinite_input_is_reported():
     with pytest.raises(Q.QttError) as ei:
         gpu_conv_full(f, g, "1d", (1e-3, 10, 1e-10), (1e-3, 8, 1e-10), (1 << 13,), 1.0)
     assert ei.value.status == Q.QTT_ENUMERIC
+
+
+@pytest.mark.parametrize("d", [2, 3, 5, 8, 11, 13, 15])
+def test_conv_full_small_sizes_match_oracle(d):
+    """The size range's low end: the one-CTA finisher path (d <= 12), the
+    per-element expansion path (d < 15), d = 2 (one cut) and odd d;
+    random data at eps = 0 (no truncation but the rank cap) and 1e-3."""
+    n = 1 << d
+    f = synth.random_signal((n,), 100 + d)
+    g = synth.random_signal((n,), 200 + d, "smooth")
+    for eps in (0.0, 1e-3):
+        dec, fft = (eps, 10, 1e-10), (eps, 8, 1e-10)
+        y, rep = gpu_conv_full(f, g, "1d", dec, fft, (n // 2,), 1.0 / n)
+        want, info = O.conv_pipeline(f, g, "1d", dec, fft, (n // 2,), 1.0 / n, return_info=True)
+        assert rep["ranks_out"] == O.ranks_of(info["Y"])
+        assert rel(y, want) <= TOL
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 6])
+def test_conv_full_small_2d_both_layouts(b):
+    """2D at 2x2 .. 64x64, interleaved and concatenated bits."""
+    n = 1 << b
+    f = synth.random_signal((n, n), 300 + b)
+    g = synth.kernel(2, b, 3.0)
+    for lay in ("interleaved", "concat"):
+        y, rep = gpu_conv_full(f, g, lay, (1e-6, 10, 1e-10), (1e-6, 8, 1e-10), (n // 2, n // 2), 1.0 / (n * n))
+        want, info = O.conv_pipeline(f, g, lay, (1e-6, 10, 1e-10), (1e-6, 8, 1e-10), (n // 2, n // 2),
+                                     1.0 / (n * n), return_info=True)
+        assert rep["ranks_out"] == O.ranks_of(info["Y"])
+        assert rel(y, want) <= TOL
+
+
+def test_constant_input_is_rank_one():
+    """A constant signal has QTT rank 1 everywhere; its periodic convolution
+    with a normalised kernel is the constant times the kernel sum, up to the
+    eps-truncations of the kernel and its spectrum (budget ~2 d eps, Q29)."""
+    d = 16
+    n = 1 << d
+    f = np.full(n, 2.5)
+    g = synth.kernel(1, d, 50.0)
+    h = 2.0 / n
+    dec, fft = (1e-3, 10, 1e-10), (1e-3, 8, 1e-10)
+    y, rep = gpu_conv_full(f, g, "1d", dec, fft, (n // 2,), h)
+    assert max(rep["ranks_f"]) == 1
+    assert rel(y, O.conv_pipeline(f, g, "1d", dec, fft, (n // 2,), h)) <= TOL
+    np.testing.assert_allclose(y, 2.5 * h * g.sum(), rtol=2 * d * 1e-3)
