@@ -282,7 +282,7 @@ qtt_status run_transform(const std::vector<XfProb>& hv, const qtt_shape* s, cons
 }
 
 qtt_status run_expand(const cplx* cores, const int* ranks, int nt, int d, double* y, long long ystride,
-                      const qtt_shape* s, int imag, Carver& cv, cudaStream_t st) {
+                      const qtt_shape* s, int imag, Carver& cv, cudaStream_t st, int rcap = RC) {
   std::vector<ExProb> h(nt);
   for (int i = 0; i < nt; ++i) {
     h[i].cores = cores + (size_t)i * d * SLOT;
@@ -292,7 +292,7 @@ qtt_status run_expand(const cplx* cores, const int* ranks, int nt, int d, double
   }
   ExProb* dp = cv.take<ExProb>(nt);
   if (!cv.base) return QTT_OK;
-  ExParams P{d, s->layout, s->bits[0], imag};
+  ExParams P{d, s->layout, s->bits[0], imag, rcap};
   qtt_status r;
   if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), nt * sizeof(ExProb), cudaMemcpyHostToDevice, st),
                       "copy descriptors")))
@@ -613,7 +613,8 @@ void plan_sharded_expand(Carver& cv, const cplx* cores, const int* ranks, const 
   E.ex_dev = cv.take<ExProb>(nlocal);
 }
 
-qtt_status run_sharded_expand(ShardEx& E, const qtt_shape* s, const ShardGeom& g, int d, int imag, cudaStream_t st) {
+qtt_status run_sharded_expand(ShardEx& E, const qtt_shape* s, const ShardGeom& g, int d, int imag, cudaStream_t st,
+                              int rcap = RC) {
   qtt_status r;
   const int n = (int)E.fp.size();
   if ((r = cuda_check(cudaMemcpyAsync(E.fp_dev, E.fp.data(), n * sizeof(FoldProb), cudaMemcpyHostToDevice, st),
@@ -623,7 +624,7 @@ qtt_status run_sharded_expand(ShardEx& E, const qtt_shape* s, const ShardGeom& g
                       "copy descriptors")))
     return r;
   if ((r = cuda_check(launch_fold_tail(E.fp_dev, n, d, g.l, st), "fold tail"))) return r;
-  ExParams P{g.dl, s->layout, g.lbits[0], imag};
+  ExParams P{g.dl, s->layout, g.lbits[0], imag, rcap};
   return cuda_check(launch_expand(E.ex_dev, n, P, st), "expand launch");
 }
 
@@ -842,7 +843,7 @@ qtt_status qtt_to_full(qtt_tt_t t, double* y, double* y_imag, void* ws, size_t w
     for (int im = 0; im < (y_imag ? 2 : 1); ++im) {
       Carver cv(ws);
       plan_sharded_expand(cv, t->cores, t->ranks, g, comm->nlocal, comm_first(comm), im ? y_imag : y, E);
-      if ((r = run_sharded_expand(E, &t->shape, g, d, im, st))) return r;
+      if ((r = run_sharded_expand(E, &t->shape, g, d, im, st, t->rcap))) return r;
     }
     return QTT_OK;
   }
@@ -852,10 +853,10 @@ qtt_status qtt_to_full(qtt_tt_t t, double* y, double* y_imag, void* ws, size_t w
   run_expand(t->cores, t->ranks, t->nt, d, y, ys, &t->shape, 0, dry, st);
   if ((r = check_ws(dry, ws, ws_bytes))) return r;
   Carver cv(ws);
-  if ((r = run_expand(t->cores, t->ranks, t->nt, d, y, ys, &t->shape, 0, cv, st))) return r;
+  if ((r = run_expand(t->cores, t->ranks, t->nt, d, y, ys, &t->shape, 0, cv, st, t->rcap))) return r;
   if (y_imag) {
     Carver cv2(ws);
-    if ((r = run_expand(t->cores, t->ranks, t->nt, d, y_imag, ys, &t->shape, 1, cv2, st))) return r;
+    if ((r = run_expand(t->cores, t->ranks, t->nt, d, y_imag, ys, &t->shape, 1, cv2, st, t->rcap))) return r;
   }
   return QTT_OK;
 }
@@ -937,8 +938,8 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   if (comm) {
     ShardEx E;
     plan_sharded_expand(cv, Y.cores, Y.ranks, geo, comm->nlocal, comm_first(comm), y, E);
-    if ((r = run_sharded_expand(E, shape, geo, d, 0, st))) return r;
-  } else if ((r = run_expand(Y.cores, Y.ranks, nf, d, y, ys, shape, 0, cv, st))) {
+    if ((r = run_sharded_expand(E, shape, geo, d, 0, st, fft->rmax))) return r;
+  } else if ((r = run_expand(Y.cores, Y.ranks, nf, d, y, ys, shape, 0, cv, st, fft->rmax))) {
     return r;
   }
   prof_mark(5, st);

@@ -101,16 +101,21 @@ static constexpr int NCOL = 1 << MB;         // 128 R columns per super-chunk
 static constexpr int TOP0 = ME + MB + 1;     // first top core (15)
 static constexpr int RSLD = NCOL + 4;        // ld of Rs rows (columns + pad)
 
+// R: rank capacity of the tensor (8 for the convolution output, Rhat <= 8;
+// 16 otherwise): fragments, tree and stack are sized by it, so the R = 8
+// variant keeps 3 CTAs per SM
+template <int R>
 struct ExSmem {
-  double Rs[32 * RSLD];       // [Re R; Im R] (KL x 64), row-major, ld RSLD
-  cplx stack[MAXD + 1][RC];   // stack[k-1] = C_k ... C_d (vector of size r_{k-1})
-  cplx tree[2][NCOL * RC];
+  double Rs[2 * R * RSLD];    // [Re R; Im R] (KL x 128), row-major, ld RSLD
+  cplx stack[MAXD + 1][R];    // stack[k-1] = C_k ... C_d (vector of size r_{k-1})
+  cplx tree[2][NCOL * R];
 };
 
-__global__ void __launch_bounds__(NT, 2) k_expand_main(const ExProb* probs, ExParams P, int per_cta) {
+template <int R>
+__global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb* probs, ExParams P, int per_cta) {
   const ExProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
-  ExSmem& S = *reinterpret_cast<ExSmem*>(smraw);
+  ExSmem<R>& S = *reinterpret_cast<ExSmem<R>*>(smraw);
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   const int d = P.d;
   const uint64_t nsup = 1ull << (d - ME - MB);
@@ -122,15 +127,16 @@ __global__ void __launch_bounds__(NT, 2) k_expand_main(const ExProb* probs, ExPa
   const int kl = (2 * r8 + 3) & ~3;
   const int ksteps = kl / 4;
   // A fragments: this warp's 4 m-blocks (rows 32 w .. 32 w + 31), all k-steps
-  double afr[4][8];
+  constexpr int KS = R / 2;            // k-steps of 4 covering 2 R
+  double afr[4][KS];
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
+    for (int ks = 0; ks < KS; ++ks) {
       int row = 32 * w + 8 * mb + (lane >> 2), col = 4 * ks + (lane & 3);
       afr[mb][ks] = (col < kl) ? pr.lsplit[row + 256 * col] : 0.0;
     }
-  if (tid < RC) S.stack[d][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
+  if (tid < R) S.stack[d][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
   uint32_t offrow[4], offcol[2];
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb) offrow[mb] = (uint32_t)qtt_offset(32 * w + 8 * mb + (lane >> 2), P.layout, P.bx);
@@ -172,11 +178,11 @@ __global__ void __launch_bounds__(NT, 2) k_expand_main(const ExProb* probs, ExPa
         const int be = vv & 1, src = vv >> 1;
         cplx s0 = czero(), s1 = czero();
 #pragma unroll
-        for (int j = 0; j < RC; j += 2) {
-          if (j < r1) s0 = cfma(core[i + r0 * be + 2 * r0 * j], vin[src * RC + j], s0);
-          if (j + 1 < r1) s1 = cfma(core[i + r0 * be + 2 * r0 * (j + 1)], vin[src * RC + j + 1], s1);
+        for (int j = 0; j < R; j += 2) {
+          if (j < r1) s0 = cfma(core[i + r0 * be + 2 * r0 * j], vin[src * R + j], s0);
+          if (j + 1 < r1) s1 = cfma(core[i + r0 * be + 2 * r0 * (j + 1)], vin[src * R + j + 1], s1);
         }
-        vout[vv * RC + i] = cadd(s0, s1);
+        vout[vv * R + i] = cadd(s0, s1);
       }
       __syncthreads();
       vin = vout;
@@ -187,8 +193,8 @@ __global__ void __launch_bounds__(NT, 2) k_expand_main(const ExProb* probs, ExPa
     for (int e = tid; e < kl * NCOL; e += NT) {
       const int row = e / NCOL, col = e % NCOL;
       double v = 0.0;
-      if (row < r8) v = vin[col * RC + row].x;
-      else if (row < 2 * r8) v = vin[col * RC + row - r8].y;
+      if (row < r8) v = vin[col * R + row].x;
+      else if (row < 2 * r8) v = vin[col * R + row - r8].y;
       S.Rs[row * RSLD + col] = v;
     }
     __syncthreads();
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(NT, 2) k_expand_main(const ExProb* probs, ExPa
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
+      for (int ks = 0; ks < KS; ++ks) {
         if (ks < ksteps) {
           const double bb = S.Rs[(4 * ks + (lane & 3)) * RSLD + 8 * nb + (lane >> 2)];
 #pragma unroll
@@ -271,8 +277,10 @@ cudaError_t launch_fold_tail(const FoldProb* probs_dev, int nprob, int d, int l,
 static constexpr size_t PREP_SMEM = 2 * 256 * RC * sizeof(cplx);
 
 cudaError_t setup_expand_kernels() {
-  cudaError_t e = cudaFuncSetAttribute(k_expand_main, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)sizeof(ExSmem));
+  cudaError_t e = cudaFuncSetAttribute(k_expand_main<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(ExSmem<8>));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_expand_main<RC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ExSmem<RC>));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_expand_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PREP_SMEM);
 }
@@ -287,12 +295,16 @@ cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& pr
   }
   k_expand_prep<<<nprob, 256, PREP_SMEM, st>>>(probs_dev, prm);
   const uint64_t nsup = 1ull << (d - ME - MB);
-  // aim for >= 2 CTAs per SM over all problems, contiguous ranges per CTA
-  uint64_t target = (uint64_t)(2 * NBLK_MAX + nprob - 1) / nprob;
+  // aim for a full wave (2 or 3 CTAs per SM) over all problems, contiguous
+  // ranges per CTA
+  const bool r8 = prm.rcap <= 8;
+  const int waves = r8 ? 3 * 148 : 2 * 148;
+  uint64_t target = (uint64_t)(waves + nprob - 1) / nprob;
   if (target < 1) target = 1;
   int per = (int)((nsup + target - 1) / target);
   int nb = (int)((nsup + per - 1) / per);
-  k_expand_main<<<dim3(nb, nprob), NT, sizeof(ExSmem), st>>>(probs_dev, prm, per);
+  if (r8) k_expand_main<8><<<dim3(nb, nprob), NT, sizeof(ExSmem<8>), st>>>(probs_dev, prm, per);
+  else k_expand_main<RC><<<dim3(nb, nprob), NT, sizeof(ExSmem<RC>), st>>>(probs_dev, prm, per);
   count_launches(2);
   return cudaGetLastError();
 }

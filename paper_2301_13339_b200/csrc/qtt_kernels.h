@@ -140,6 +140,7 @@ struct ExParams {
   int layout;
   int bx;
   int imag;          // 0: y = Re(full), 1: y = Im(full)
+  int rcap;          // upper bound of the ranks (selects the kernel variant)
 };
 cudaError_t setup_expand_kernels();
 cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& prm, cudaStream_t st);
