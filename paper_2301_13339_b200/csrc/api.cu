@@ -23,6 +23,17 @@ using namespace qtt;
 namespace qtt {
 static std::atomic<long long> g_launches{0};
 void count_launches(int n) { g_launches += n; }
+int sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int v = cache[dev].load();
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev].store(v);
+  }
+  return v;
+}
 }  // namespace qtt
 
 #define QTT_XSTR(x) #x

@@ -298,7 +298,7 @@ cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& pr
   // aim for a full wave (2 or 3 CTAs per SM) over all problems, contiguous
   // ranges per CTA
   const bool r8 = prm.rcap <= 8;
-  const int waves = r8 ? 3 * 148 : 2 * 148;
+  const int waves = (r8 ? 3 : 2) * sm_count();
   uint64_t target = (uint64_t)(waves + nprob - 1) / nprob;
   if (target < 1) target = 1;
   int per = (int)((nsup + target - 1) / target);

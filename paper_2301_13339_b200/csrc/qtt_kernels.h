@@ -11,6 +11,8 @@ namespace qtt {
 
 // number of kernels launched by this library (bench evidence: gpu_launches)
 void count_launches(int n);
+// SMs of the current device (cached per device; grids are sized from it)
+int sm_count();
 
 // A TT core slot holds up to RC x 2 x RC complex entries (RC = 16), stored
 // compact column-major: element (a, be, b) of an (r0, 2, r1) core at

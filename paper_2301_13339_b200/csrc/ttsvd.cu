@@ -908,13 +908,13 @@ __global__ void __launch_bounds__(NT) k_gather_w(const DecProb* sh, const DecPro
   }
 }
 
-// CTAs per problem of a full-array pass: the whole launch targets
-// GRID_TARGET CTAs (4 per SM) however many problems it carries, so batched
+// CTAs per problem of a full-array pass: the whole launch targets 4 CTAs
+// per SM of the device however many problems it carries, so batched
 // launches keep several chunks per CTA (the cp.async double buffer reaches
 // steady state) and write few per-CTA partial Grams (8 KiB each).
-static constexpr int GRID_TARGET = 4 * 148;
 static inline int per_problem(uint64_t nchunks, int nprob) {
-  uint64_t want = (uint64_t)((GRID_TARGET + nprob - 1) / nprob);
+  const int grid_target = 4 * sm_count();
+  uint64_t want = (uint64_t)((grid_target + nprob - 1) / nprob);
   if (want > (uint64_t)NBLK_MAX) want = NBLK_MAX;
   if (want > nchunks) want = nchunks;
   return want < 1 ? 1 : (int)want;
