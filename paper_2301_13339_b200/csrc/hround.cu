@@ -127,9 +127,6 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     }
     __syncthreads();
   }
-#ifdef QTT_HR_GR_ONLY
-  return;   // timing experiment only: right Gram chain alone
-#endif
   // ---------------- LQ rank bounds
   if (tid == 0) {
     S.rb[d] = 1;
