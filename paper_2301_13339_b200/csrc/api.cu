@@ -266,7 +266,8 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
 }
 
 qtt_status run_transform(const std::vector<XfProb>& hv, const qtt_shape* s, const qtt_trunc* fft, int inverse,
-                         const long long* shift, double scale, Carver& cv, int* status, cudaStream_t st) {
+                         const long long* shift, double scale, Carver& cv, int* status, cudaStream_t st,
+                         int rs = RS_XF) {
   const int n = (int)hv.size();
   XfProb* dp = cv.take<XfProb>(n);
   if (!cv.base) return QTT_OK;
@@ -280,6 +281,7 @@ qtt_status run_transform(const std::vector<XfProb>& hv, const qtt_shape* s, cons
   P.ctol = fft->cluster_tol;
   P.rule = fft->rule;
   P.delta = fft->delta;
+  P.rs = rs;
   P.inverse = inverse;
   P.scale = inverse ? scale * ldexp(1.0, -P.d) : 1.0;
   P.shift[0] = shift ? shift[0] : 0;
@@ -328,7 +330,8 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.in_ranks = (isf ? fr : gr) + (size_t)j * 64;
     p.out_cores = (isf ? Fh.cores : Gh.cores) + (size_t)j * d * SLOT;
     p.out_ranks = (isf ? Fh.ranks : Gh.ranks) + (size_t)j * 64;
-    p.gr = cv.take<cplx>((size_t)MAXD * GR_XF);
+    p.gr = cv.take<cplx>((size_t)MAXD * xf_gr_slot(RS_XF));
+    p.cwork = nullptr;
     p.do_center = (!isf && shift) ? 1 : 0;   // center the kernel's spectrum only (O3)
   }
   // forward transforms of all F's and G's: one launch, one CTA each
@@ -356,6 +359,7 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.out_cores = Y.cores + (size_t)i * d * SLOT;
     p.out_ranks = Y.ranks + (size_t)i * 64;
     p.gr = fw[i].gr;   // reuse the forward scratch
+    p.cwork = nullptr;
     p.do_center = 0;
   }
   if (cv.base) {
@@ -778,11 +782,13 @@ qtt_status qtt_transform(qtt_tt_t in, const qtt_trunc* fft, int inverse, const l
                          void* ws, size_t ws_bytes, void* stream, qtt_tt_t* out) {
   qtt_status r;
   if (!in || !out) return fail(QTT_EINVAL, "in / out is NULL");
-  if ((r = check_trunc(fft, RS_XF, "fft"))) return r;
-  if (in->rcap > RS_XF) return fail(QTT_EINVAL, "input ranks may exceed %d", RS_XF);
+  if ((r = check_trunc(fft, RS_BIG, "fft"))) return r;
+  if (in->rcap > RS_BIG) return fail(QTT_EINVAL, "input ranks may exceed %d", RS_BIG);
   cudaError_t ce;
   if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
   const int d = in->d, n = in->nt;
+  // the shared-memory variant holds ranks <= RS_XF; above that the cores live in the workspace
+  const int rs = (in->rcap > RS_XF || fft->rmax > RS_XF) ? RS_BIG : RS_XF;
   cudaStream_t st = (cudaStream_t)stream;
   auto plan = [&](Carver& cv, TTAlloc& o, std::vector<XfProb>& v) {
     o = take_tt(cv, n, d);
@@ -792,7 +798,8 @@ qtt_status qtt_transform(qtt_tt_t in, const qtt_trunc* fft, int inverse, const l
       v[i].in_ranks = in->ranks + (size_t)i * 64;
       v[i].out_cores = o.cores + (size_t)i * d * SLOT;
       v[i].out_ranks = o.ranks + (size_t)i * 64;
-      v[i].gr = cv.take<cplx>((size_t)MAXD * GR_XF);
+      v[i].gr = cv.take<cplx>((size_t)MAXD * xf_gr_slot(rs));
+      v[i].cwork = rs == RS_BIG ? cv.take<cplx>((size_t)MAXD * 2 * RS_BIG * RS_BIG) : nullptr;
       v[i].do_center = (!inverse && shift) ? 1 : 0;
     }
   };
@@ -800,11 +807,11 @@ qtt_status qtt_transform(qtt_tt_t in, const qtt_trunc* fft, int inverse, const l
   TTAlloc o;
   std::vector<XfProb> v;
   plan(dry, o, v);
-  run_transform(v, &in->shape, fft, inverse, shift, scale, dry, nullptr, st);
+  run_transform(v, &in->shape, fft, inverse, shift, scale, dry, nullptr, st, rs);
   if ((r = check_ws(dry, ws, ws_bytes))) return r;
   Carver cv(ws);
   plan(cv, o, v);
-  if ((r = run_transform(v, &in->shape, fft, inverse, shift, scale, cv, in->status, st))) return r;
+  if ((r = run_transform(v, &in->shape, fft, inverse, shift, scale, cv, in->status, st, rs))) return r;
   *out = new_handle(&in->shape, n, fft->rmax, o, in->status, st);
   return *out ? QTT_OK : fail(QTT_ENOMEM, "host allocation failed");
 }

@@ -22,7 +22,6 @@
 namespace qtt {
 
 static constexpr int NT = 256;
-static constexpr int RS = RS_XF;
 
 // optional phase timing (compile with -DQTT_XF_TIMING): cycles per phase of
 // CTA 0 are accumulated into XfProb::gr scratch tail (debug builds only)
@@ -35,22 +34,29 @@ static constexpr int RS = RS_XF;
 #define XT_MARK(k)
 #define XT_DUMP(ptr)
 #endif
-static constexpr int CSZ = 2 * RS * RS;
-static constexpr int R2 = 2 * RS;
-
-struct XfSmem {
-  cplx C[MAXD][CSZ];
+// Rank capacity RSV of the compact cores: 10 (Rhat <= 8 pipelines; every
+// core in shared memory) or 16 (the paper's Rhat = 15; the cores live in the
+// workspace, pr.cwork, and stay L2-resident).  Rows of a cut <= 2 RSV.
+template <int RSV>
+struct XfBufs {
+  static constexpr int R2 = 2 * RSV;
   cplx D[R2 * 2 * R2];
-  cplx Eb[RS * 2 * R2];
+  cplx Eb[RSV * 2 * R2];
   cplx G[2][R2 * R2];
   cplx T[2 * R2 * R2];
-  cplx Sm[RS * R2];
+  cplx Sm[RSV * R2];
   EigSmem<R2> E;
   int r[MAXD + 1];
   int rb[MAXD + 1];
   int rk;
   double tau2;
 };
+template <int RSV, bool SMEM_CORES = (RSV <= 10)>
+struct XfSmem : XfBufs<RSV> {
+  cplx C[MAXD][2 * RSV * RSV];
+};
+template <int RSV>
+struct XfSmem<RSV, false> : XfBufs<RSV> {};
 
 // twiddle of position q (1-based) in the stage of axis a, bit t, slice be
 __device__ __forceinline__ cplx phi_of(const XfParams& P, int q, int a, int t, int be) {
@@ -61,10 +67,10 @@ __device__ __forceinline__ cplx phi_of(const XfParams& P, int q, int a, int t, i
 
 // doubled core of position q (p < q <= d) of the current stage into S.D;
 // dims (2 a0) x 2 x (q < d ? 2 b0 : 1)
-__device__ void build_doubled(XfSmem& S, const XfParams& P, int q, int a, int t) {
+template <class SM>
+__device__ void build_doubled(SM& S, const cplx* c, const XfParams& P, int q, int a, int t) {
   const int d = P.d;
   const int a0 = S.r[q - 1], b0 = S.r[q];
-  const cplx* c = S.C[q - 1];
   const cplx ph = phi_of(P, q, a, t, 1);
   if (q < d) {
     const int rows = 2 * a0, cols = 2 * b0;
@@ -89,11 +95,17 @@ __device__ void build_doubled(XfSmem& S, const XfParams& P, int q, int a, int t)
   }
 }
 
+template <int RSV>
 __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams P) {
   const XfProb& pr = probs[blockIdx.x];
   extern __shared__ __align__(16) unsigned char smraw[];
-  XfSmem& S = *reinterpret_cast<XfSmem*>(smraw);
+  XfSmem<RSV>& S = *reinterpret_cast<XfSmem<RSV>*>(smraw);
+  constexpr int RS = RSV, R2 = 2 * RSV, CSZ = 2 * RSV * RSV, GRS = R2 * R2;
   constexpr int LD = EigSmem<R2>::LD;
+  auto core = [&](int q) -> cplx* {
+    if constexpr (RSV <= 10) return S.C[q];
+    else return pr.cwork + (size_t)q * CSZ;
+  };
   const int tid = threadIdx.x;
   const int d = P.d;
   // load (conj for the inverse)
@@ -103,7 +115,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
     const int n = S.r[q] * 2 * S.r[q + 1];
     for (int e = tid; e < n; e += NT) {
       cplx v = pr.in_cores[(size_t)q * SLOT + e];
-      S.C[q][e] = P.inverse ? cconj(v) : v;
+      core(q)[e] = P.inverse ? cconj(v) : v;
     }
   }
   __syncthreads();
@@ -112,7 +124,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
     const int a = P.axis[p - 1], t = P.bit[p - 1];
     if (p == d) {
       const int a0 = S.r[d - 1];
-      cplx* c = S.C[d - 1];
+      cplx* c = core(d - 1);
       for (int i = tid; i < a0; i += NT) {
         cplx x0 = c[i], x1 = c[i + a0];
         c[i] = cadd(x0, x1);
@@ -122,7 +134,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       continue;
     }
     // ---- right Gram chain GR_c, c = d-1 .. p, into global slots
-    build_doubled(S, P, d, a, t);
+    build_doubled(S, core(d - 1), P, d, a, t);
     __syncthreads();
     {
       const int rows = 2 * S.r[d - 1];
@@ -131,13 +143,13 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
         cplx s = czero();
         for (int be = 0; be < 2; ++be) s = cfma_bc(S.D[i + rows * be], S.D[j + rows * be], s);
         S.G[0][e] = s;
-        pr.gr[(size_t)(d - 1) * GR_XF + e] = s;
+        pr.gr[(size_t)(d - 1) * GRS + e] = s;
       }
     }
     __syncthreads();
     int gc = 0;
     for (int c = d - 1; c >= p + 1; --c) {
-      build_doubled(S, P, c, a, t);
+      build_doubled(S, core(c - 1), P, c, a, t);
       __syncthreads();
       const int rows = 2 * S.r[c - 1], cols = 2 * S.r[c];
       // T[be] = D[be] G   (rows x cols)
@@ -157,7 +169,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
           for (int l = 0; l < cols; ++l)
             s = cfma_bc(S.T[i + rows * l + rows * cols * be], S.D[j + rows * be + 2 * rows * l], s);
         S.G[gc ^ 1][e] = s;
-        pr.gr[(size_t)(c - 1) * GR_XF + e] = s;
+        pr.gr[(size_t)(c - 1) * GRS + e] = s;
       }
       __syncthreads();
       gc ^= 1;
@@ -174,7 +186,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
     // ---- E = concat(core_p)
     {
       const int a0 = S.r[p - 1], b0 = S.r[p];
-      const cplx* c = S.C[p - 1];
+      const cplx* c = core(p - 1);
       for (int e = tid; e < a0 * 2 * 2 * b0; e += NT) {
         int i = e % a0, al = (e / a0) & 1, j = e / (2 * a0);
         cplx v = (j < b0) ? c[i + 2 * a0 * j] : c[i + a0 + 2 * a0 * (j - b0)];
@@ -188,7 +200,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
     for (int c = p; c <= d - 1; ++c) {
       const int rows = 2 * ap, cols = 2 * S.r[c];
       XT_MARK(5)
-      for (int e = tid; e < cols * cols; e += NT) S.G[0][e] = pr.gr[(size_t)c * GR_XF + e];
+      for (int e = tid; e < cols * cols; e += NT) S.G[0][e] = pr.gr[(size_t)c * GRS + e];
       __syncthreads();
       // T = M G  (rows x cols), M = Eb (ld rows)
       for (int e = tid; e < rows * cols; e += NT) {
@@ -226,7 +238,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       // new core c = U_r  (ap x 2 x rk)
       for (int e = tid; e < rows * rk; e += NT) {
         int i = e % rows, r = e / rows;
-        S.C[c - 1][i + rows * r] = U[i + LD * r];
+        core(c - 1)[i + rows * r] = U[i + LD * r];
       }
       // Sm = U_r^H M  (rk x cols)
       for (int e = tid; e < rk * cols; e += NT) {
@@ -240,7 +252,7 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       {
         const int q = c + 1;
         const int a1 = S.r[c];
-        const cplx* cn = S.C[q - 1];
+        const cplx* cn = core(q - 1);
         if (q < d) {
           const int b1 = S.r[q];
           for (int e = tid; e < rk * 2 * 2 * b1; e += NT) {
@@ -274,16 +286,16 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
       ap = rk;
       XT_MARK(3)
     }
-    for (int e = tid; e < ap * 2; e += NT) S.C[d - 1][e] = S.Eb[e];
+    for (int e = tid; e < ap * 2; e += NT) core(d - 1)[e] = S.Eb[e];
     __syncthreads();
   }
   XT_MARK(4)
-  XT_DUMP(pr.gr + (size_t)MAXD * GR_XF - 8)
+  XT_DUMP(pr.gr + (size_t)MAXD * GRS - 8)
   // ---- reversal (core'_q = core_{d+1-q}, rank indices swapped), center,
   //      conj (inverse), scale core 1
   for (int q = tid; q <= d; q += NT) pr.out_ranks[q] = S.r[d - q];
   for (int q = 1; q <= d; ++q) {
-    const cplx* c = S.C[d - q];
+    const cplx* c = core(d - q);
     const int a0 = S.r[d - q], b0 = S.r[d - q + 1];   // source dims (a0, 2, b0)
     cplx ph = cmk(1.0, 0.0);
     if (pr.do_center) {
@@ -305,11 +317,18 @@ __global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams 
 }
 
 cudaError_t setup_xf_kernels() {
-  return cudaFuncSetAttribute(k_transform, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(XfSmem));
+  cudaError_t e = cudaFuncSetAttribute(k_transform<RS_XF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(XfSmem<RS_XF>));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_transform<RS_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)sizeof(XfSmem<RS_BIG>));
 }
 
+size_t xf_gr_slot(int rs) { return (size_t)(2 * rs) * (2 * rs); }
+
 cudaError_t launch_transform(const XfProb* probs_dev, int nprob, const XfParams& prm, cudaStream_t st) {
-  k_transform<<<nprob, NT, sizeof(XfSmem), st>>>(probs_dev, prm);
+  if (prm.rs > RS_XF) k_transform<RS_BIG><<<nprob, NT, sizeof(XfSmem<RS_BIG>), st>>>(probs_dev, prm);
+  else k_transform<RS_XF><<<nprob, NT, sizeof(XfSmem<RS_XF>), st>>>(probs_dev, prm);
   count_launches(1);
   return cudaGetLastError();
 }

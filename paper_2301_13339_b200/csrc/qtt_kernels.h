@@ -23,6 +23,7 @@ static constexpr int SLOT = 2 * RC * RC;
 static constexpr int NBLK_MAX = 296;      // 2 x 148 SMs
 static constexpr int MAXD = 30;
 static constexpr int RS_XF = 10;          // compact rank capacity of the transform kernels
+static constexpr int RS_BIG = 16;         // ... of the large-capacity variant (Rhat up to 16)
 static constexpr int RH_MAX = 8;          // Rhat cap supported by the Hadamard rounding
 
 // ---------------------------------------------------------------- TT-SVD
@@ -85,8 +86,9 @@ struct XfProb {
   const int* in_ranks;
   cplx* out_cores;
   int* out_ranks;
-  cplx* gr;          // right-Gram scratch: MAXD slots of (2 RS_XF)^2
+  cplx* gr;          // right-Gram scratch: MAXD slots of (2 rs)^2 (xf_gr_slot)
   int do_center;     // multiply the forward output by the centering phase (O3)
+  cplx* cwork;       // rs = RS_BIG only: MAXD compact cores of 2 RS_BIG^2
 };
 struct XfParams {
   int d;
@@ -102,8 +104,10 @@ struct XfParams {
   int* status;
   int rule;
   double delta;
+  int rs;            // rank capacity variant: RS_XF or RS_BIG
 };
-static constexpr int GR_XF = 4 * RS_XF * RS_XF;   // complex per GR slot
+static constexpr int GR_XF = 4 * RS_XF * RS_XF;   // complex per GR slot (rs = RS_XF)
+size_t xf_gr_slot(int rs);                        // complex per GR slot of a variant
 cudaError_t setup_xf_kernels();
 cudaError_t launch_transform(const XfProb* probs_dev, int nprob, const XfParams& prm, cudaStream_t st);
 
