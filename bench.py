@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-fft-comparator", action="store_true")
     ap.add_argument("--ref-step-seconds", type=float, default=None,
                     help="--impl reference: CPU seconds per step (default: ~60 s over the whole run)")
+    ap.add_argument("--rhat", type=int, default=None,
+                    help="override the QTT-FFT / rounding cap Rhat_max (default 8, reading Q4; paper 15)")
     return ap.parse_args()
 
 
@@ -521,6 +523,8 @@ def run_reference(a):
 
 def main():
     a = parse()
+    if a.rhat is not None:
+        synth.R_HAT = a.rhat
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -73,7 +73,10 @@ typedef struct {
 } qtt_shape;
 
 /* Truncation policy: eps >= 0, 1 <= rmax <= 16, cluster_tol >= 0.
- * Decomposition caps use rmax (R_max); transform/rounding caps Rhat.
+ * Decomposition caps use rmax (R_max <= 10); transform/rounding caps Rhat
+ * (<= 16; the paper's Rhat_max = 15).  Rhat <= 8 runs the
+ * one-CTA Hadamard rounding, 9..16 the multi-CTA one (Kronecker ranks of
+ * F (.) G up to 160 resp. 256).
  * rule = QTT_RULE_EPS (0): r = RANK(eps, rmax, cluster_tol) — modification
  *   (1), tau^2 = eps^2 ||A||^2 / (d-1);
  * rule = QTT_RULE_DROPOFF (1): SV drop-off, modification (3), P:363-365:

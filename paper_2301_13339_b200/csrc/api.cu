@@ -104,6 +104,7 @@ cudaError_t setup_all() {
     if ((e = setup_ttsvd_kernels()) != cudaSuccess) { g_setup_err = e; return; }
     if ((e = setup_xf_kernels()) != cudaSuccess) { g_setup_err = e; return; }
     if ((e = setup_hr_kernels()) != cudaSuccess) { g_setup_err = e; return; }
+    if ((e = setup_hr_big_kernels()) != cudaSuccess) { g_setup_err = e; return; }
     if ((e = setup_expand_kernels()) != cudaSuccess) { g_setup_err = e; return; }
   });
   return g_setup_err;
@@ -318,6 +319,9 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
                         const qtt_shape* s, const qtt_trunc* fft, const long long* shift, double scale,
                         TTAlloc Y, Carver& cv, int* status, cudaStream_t st) {
   const int d = shape_d(s);
+  // Rhat <= RH_MAX: one-CTA rounding; above: the multi-CTA variant (Kronecker ranks <= 256)
+  const bool big = fft->rmax > RH_MAX;
+  const int rs = fft->rmax > RS_XF ? RS_BIG : RS_XF;
   TTAlloc Fh = take_tt(cv, nf, d);
   TTAlloc Gh = take_tt(cv, ng, d);
   TTAlloc Z = take_tt(cv, nf, d);
@@ -330,27 +334,52 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.in_ranks = (isf ? fr : gr) + (size_t)j * 64;
     p.out_cores = (isf ? Fh.cores : Gh.cores) + (size_t)j * d * SLOT;
     p.out_ranks = (isf ? Fh.ranks : Gh.ranks) + (size_t)j * 64;
-    p.gr = cv.take<cplx>((size_t)MAXD * xf_gr_slot(RS_XF));
-    p.cwork = nullptr;
+    p.gr = cv.take<cplx>((size_t)MAXD * xf_gr_slot(rs));
+    p.cwork = rs == RS_BIG ? cv.take<cplx>((size_t)MAXD * 2 * RS_BIG * RS_BIG) : nullptr;
     p.do_center = (!isf && shift) ? 1 : 0;   // center the kernel's spectrum only (O3)
   }
   // forward transforms of all F's and G's: one launch, one CTA each
   qtt_status r;
-  if ((r = run_transform(fw, s, fft, 0, shift, 1.0, cv, status, st))) return r;
+  if ((r = run_transform(fw, s, fft, 0, shift, 1.0, cv, status, st, rs))) return r;
   if (cv.base) prof_mark(2, st);
-  std::vector<HrProb> hr(nf);
+  std::vector<HrProb> hr(big ? 0 : nf);
+  std::vector<HrBigProb> hb(big ? nf : 0);
   for (int i = 0; i < nf; ++i) {
-    HrProb& p = hr[i];
+    const int j = ng == 1 ? 0 : i;
+    if (!big) {
+      HrProb& p = hr[i];
+      p.f_cores = Fh.cores + (size_t)i * d * SLOT;
+      p.f_ranks = Fh.ranks + (size_t)i * 64;
+      p.g_cores = Gh.cores + (size_t)j * d * SLOT;
+      p.g_ranks = Gh.ranks + (size_t)j * 64;
+      p.out_cores = Z.cores + (size_t)i * d * SLOT;
+      p.out_ranks = Z.ranks + (size_t)i * 64;
+      p.gr = cv.take<cplx>((size_t)MAXD * GR_HR);
+      continue;
+    }
+    HrBigProb& p = hb[i];
     p.f_cores = Fh.cores + (size_t)i * d * SLOT;
     p.f_ranks = Fh.ranks + (size_t)i * 64;
-    const int j = ng == 1 ? 0 : i;
     p.g_cores = Gh.cores + (size_t)j * d * SLOT;
     p.g_ranks = Gh.ranks + (size_t)j * 64;
     p.out_cores = Z.cores + (size_t)i * d * SLOT;
     p.out_ranks = Z.ranks + (size_t)i * 64;
-    p.gr = cv.take<cplx>((size_t)MAXD * GR_HR);
+    constexpr size_t Q2 = (size_t)RH_BIG * RH_BIG * RH_BIG * RH_BIG;   // 256 x 256
+    constexpr size_t EW = (size_t)2 * RH_BIG * RH_BIG * RH_BIG;        // 32 x 256
+    cplx* base = cv.take<cplx>(hr_big_scratch(d));
+    p.gr = base;
+    p.t1 = base + (size_t)d * Q2;
+    p.t2 = p.t1 + 2 * Q2;
+    p.t3 = p.t2 + 2 * Q2;
+    p.e = p.t3 + 2 * Q2;
+    p.tb = p.e + EW;
+    p.sm = p.tb + EW;
+    p.hb = p.sm + EW;
+    p.st = cv.take<int>(128);
+    p.tau2 = cv.take<double>(1);
   }
-  HrProb* hp = cv.take<HrProb>(nf);
+  HrProb* hp = big ? nullptr : cv.take<HrProb>(nf);
+  HrBigProb* hbp = big ? cv.take<HrBigProb>(nf) : nullptr;
   std::vector<XfProb> iv(nf);
   for (int i = 0; i < nf; ++i) {
     XfProb& p = iv[i];
@@ -359,18 +388,25 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.out_cores = Y.cores + (size_t)i * d * SLOT;
     p.out_ranks = Y.ranks + (size_t)i * 64;
     p.gr = fw[i].gr;   // reuse the forward scratch
-    p.cwork = nullptr;
+    p.cwork = fw[i].cwork;
     p.do_center = 0;
   }
   if (cv.base) {
     HrParams H{d, fft->eps, fft->rmax, fft->cluster_tol, status, fft->rule, fft->delta};
-    if ((r = cuda_check(cudaMemcpyAsync(hp, hr.data(), nf * sizeof(HrProb), cudaMemcpyHostToDevice, st),
-                        "copy descriptors")))
-      return r;
-    if ((r = cuda_check(launch_hadamard_round(hp, nf, H, st), "hadamard/round launch"))) return r;
+    if (big) {
+      if ((r = cuda_check(cudaMemcpyAsync(hbp, hb.data(), nf * sizeof(HrBigProb), cudaMemcpyHostToDevice, st),
+                          "copy descriptors")))
+        return r;
+      if ((r = cuda_check(launch_hadamard_round_big(hbp, nf, H, st), "hadamard/round launch"))) return r;
+    } else {
+      if ((r = cuda_check(cudaMemcpyAsync(hp, hr.data(), nf * sizeof(HrProb), cudaMemcpyHostToDevice, st),
+                          "copy descriptors")))
+        return r;
+      if ((r = cuda_check(launch_hadamard_round(hp, nf, H, st), "hadamard/round launch"))) return r;
+    }
     prof_mark(3, st);
   }
-  r = run_transform(iv, s, fft, 1, nullptr, scale, cv, status, st);
+  r = run_transform(iv, s, fft, 1, nullptr, scale, cv, status, st, rs);
   if (cv.base) prof_mark(4, st);
   return r;
 }
@@ -702,7 +738,7 @@ const char* qtt_build_info(void) {
 }
 
 size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const qtt_trunc* fft, int nranks) {
-  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec", true) || check_trunc(fft, RH_MAX, "fft") || nranks < 1)
+  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec", true) || check_trunc(fft, RH_BIG, "fft") || nranks < 1)
     return 0;
   if (nranks > 1 && dec->rule == QTT_RULE_RSVD) return 0;
   if (nranks > 1) return ws_sharded(shape, fft, nranks, 1);
@@ -724,7 +760,7 @@ size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const q
 size_t qtt_comm_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const qtt_trunc* fft,
                                 qtt_comm_t comm) {
   if (!comm) return qtt_workspace_bytes(shape, dec, fft, 1);
-  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec") || check_trunc(fft, RH_MAX, "fft")) return 0;
+  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec") || check_trunc(fft, RH_BIG, "fft")) return 0;
   return ws_sharded(shape, fft, comm->nshards, comm->nlocal);
 }
 
@@ -820,7 +856,7 @@ qtt_status qtt_convolve(qtt_tt_t f, qtt_tt_t g, const qtt_trunc* fft, const long
                         void* ws, size_t ws_bytes, void* stream, qtt_tt_t* out) {
   qtt_status r;
   if (!f || !g || !out) return fail(QTT_EINVAL, "f / g / out is NULL");
-  if ((r = check_trunc(fft, RH_MAX, "fft"))) return r;
+  if ((r = check_trunc(fft, RH_BIG, "fft"))) return r;
   if (f->d != g->d) return fail(QTT_EINVAL, "f and g have different d");
   if (g->nt != 1 && g->nt != f->nt) return fail(QTT_EINVAL, "g must hold 1 tensor or as many as f");
   if (f->rcap > RS_XF || g->rcap > RS_XF) return fail(QTT_EINVAL, "input ranks may exceed %d", RS_XF);
@@ -885,7 +921,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   qtt_status r;
   if ((r = check_shape(shape))) return r;
   if ((r = check_trunc(dec, RS_XF, "dec", !comm))) return r;
-  if ((r = check_trunc(fft, RH_MAX, "fft"))) return r;
+  if ((r = check_trunc(fft, RH_BIG, "fft"))) return r;
   if (!f || !g || !y) return fail(QTT_EINVAL, "f / g / y is NULL");
   ShardGeom geo{};
   if (comm && (r = check_comm(comm, shape, &geo))) return r;

@@ -24,7 +24,8 @@ static constexpr int NBLK_MAX = 296;      // 2 x 148 SMs
 static constexpr int MAXD = 30;
 static constexpr int RS_XF = 10;          // compact rank capacity of the transform kernels
 static constexpr int RS_BIG = 16;         // ... of the large-capacity variant (Rhat up to 16)
-static constexpr int RH_MAX = 8;          // Rhat cap supported by the Hadamard rounding
+static constexpr int RH_MAX = 8;          // Rhat cap of the one-CTA Hadamard rounding (hround.cu)
+static constexpr int RH_BIG = 16;         // ... of the multi-CTA variant (hround_big.cu)
 
 // ---------------------------------------------------------------- TT-SVD
 struct DecProb {
@@ -133,6 +134,29 @@ struct HrParams {
 static constexpr int GR_HR = 64 * 64;
 cudaError_t setup_hr_kernels();
 cudaError_t launch_hadamard_round(const HrProb* probs_dev, int nprob, const HrParams& prm, cudaStream_t st);
+
+// Rhat up to RH_BIG: Kronecker ranks up to 256, scratch in the workspace
+struct HrBigProb {
+  const cplx* f_cores;
+  const int* f_ranks;
+  const cplx* g_cores;
+  const int* g_ranks;
+  cplx* out_cores;
+  int* out_ranks;
+  cplx* gr;          // d slots of 256 x 256 (right Grams of Z)
+  cplx* t1;          // 2 slices x 256 x 256 each: mode-product intermediates
+  cplx* t2;
+  cplx* t3;
+  cplx* e;           // E of the current cut: rows x rz (rows <= 32, rz <= 256)
+  cplx* tb;          // T = E GR
+  cplx* sm;          // U_r^H E
+  cplx* hb;          // Sm x G
+  int* st;           // sweep state (ranks, LQ bounds)
+  double* tau2;
+};
+cudaError_t setup_hr_big_kernels();
+size_t hr_big_scratch(int d);   // complex entries of gr + t1..t3 + e, tb, sm, hb
+cudaError_t launch_hadamard_round_big(const HrBigProb* probs_dev, int nprob, const HrParams& prm, cudaStream_t st);
 
 // -------------------------------------------------------------- expansion
 struct ExProb {

@@ -6,7 +6,7 @@ to 2^K per axis, kernel eq. sinc_kern1/2, linear
 paper's rank 26).
 
 Through the C ABI with caps (R_max, Rhat_max) = (10, 8) (reading Q4; the
-paper's Rhat = 15 needs a rank-225 rounding kernel, not in this build):
+paper's own caps (10, 15) are in test_gpu_rhat15.py):
 identical ranks and rel-L2 <= 1e-9 against the oracle on the same inputs, and
 the Table 1 quality regime: E2 of the QTT result against the exact
 convolution of the clean signal well below E2 of the dense FFT of the noisy

@@ -1,6 +1,13 @@
 """The paper's cap Rhat_max = 15: the
 large-capacity transform variant (compact cores of rank <= 16 in the
-workspace, 32-wide eigensolver) against the oracle, forward and inverse."""
+workspace, 32-wide eigensolver) against the oracle, forward and inverse; and
+the multi-CTA Hadamard rounding (Kronecker ranks up to 256) end to end, at
+the paper's own caps (R_max, Rhat_max) = (10, 15) on its worked examples —
+identical ranks, rel-L2 <= 1e-9 against the oracle, and Table 1's I_QTT0
+(P:596-598)."""
+
+import json
+import os
 
 import numpy as np
 import pytest
@@ -8,7 +15,7 @@ import pytest
 import oracle as O
 from paper_2301_13339_b200 import synth
 
-from gpu_util import gpu_full, gpu_transform, gpu_tt_from_cores
+from gpu_util import gpu_conv_full, gpu_full, gpu_transform, gpu_tt_from_cores
 
 pytestmark = pytest.mark.gpu
 
@@ -42,3 +49,58 @@ def test_transform_rhat15_parity(name, make, layout, eps):
     ti = gpu_transform(gpu_tt_from_cores(Fh, x, layout, rcap=16), None, eps, 15, inverse=True)
     assert ti.ranks() == O.ranks_of(Y)
     assert rel(gpu_full(ti, x, imag=True), O.from_qtt(O.full(Y), x.shape, lay)) <= 1e-9
+
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_pins.json")))
+
+
+def fft_conv(f, g, shift, scale):
+    D = f.ndim
+    gs = np.roll(g, tuple(-s for s in shift[::-1]), axis=tuple(range(D)))
+    return scale * np.real(np.fft.ifftn(np.fft.fftn(f) * np.fft.fftn(gs)))
+
+
+@pytest.mark.parametrize("num,K,key", [(1, 20, "example1_K20"), (2, 20, "example2_K20"),
+                                       (3, 10, "example3_K10")])
+def test_conv_paper_caps_table1(num, K, key):
+    ex = synth.paper_example(num, K, noisy=True, seed=0)
+    cl = synth.paper_example(num, K, noisy=False)
+    lay = "1d" if ex["D"] == 1 else "concat"
+    dec, fft = (1e-3, 10, 1e-10), (1e-3, 15, 1e-10)
+    y, rep = gpu_conv_full(ex["f"], ex["g"], lay, dec, fft, ex["shift"], ex["scale"])
+    want, info = O.conv_pipeline(ex["f"], ex["g"], lay, dec, fft, ex["shift"], ex["scale"], return_info=True)
+    assert rep["status_bits"] & 3 == 0
+    assert rep["ranks_f"] == O.ranks_of(info["F"])
+    assert rep["ranks_g"] == O.ranks_of(info["G"])
+    assert rep["ranks_out"] == O.ranks_of(info["Y"])
+    assert np.linalg.norm(y - want) <= 1e-9 * np.linalg.norm(want)
+    sl = (slice(0, ex["N"]),) * ex["D"]
+    ref = fft_conv(cl["f"], cl["g"], ex["shift"], ex["scale"])[sl]
+    e = np.linalg.norm(y[sl] - ref) / np.linalg.norm(ref)
+    gold = GOLD["table1_E2"][key]
+    assert 0.25 * gold["I_QTT0"] <= e <= 2.0 * gold["I_QTT0"]
+
+
+@pytest.mark.parametrize("rhat", [9, 12, 16])
+@pytest.mark.parametrize("layout", ["interleaved", "concat", "1d"])
+def test_conv_big_rounding_caps(rhat, layout):
+    """Every cap of the multi-CTA rounding (9, 10 with the shared-memory
+    transform, 12, 16 with the workspace one), a batch of 2 with a shared
+    kernel, noisy data so the caps bind."""
+    if layout == "1d":
+        f = np.stack([synth.random_signal((1 << 12,), 70 + i) for i in range(2)])
+        g = synth.random_signal((1 << 12,), 79)
+        shift = (1 << 11, 0)
+    else:
+        f = np.stack([synth.random_signal((64, 64), 80 + i) for i in range(2)])
+        g = synth.random_signal((64, 64), 89)
+        shift = (32, 32)
+    dec, fft = (1e-6, 10, 1e-10), (1e-6, rhat, 1e-10)
+    y, rep = gpu_conv_full(f, g, layout, dec, fft, shift, 0.5, batch=2)
+    assert rep["status_bits"] & 3 == 0
+    for i in range(2):
+        want, info = O.conv_pipeline(f[i], g, layout, dec, fft, shift, 0.5, return_info=True)
+        if i == 0:
+            assert rep["ranks_out"] == O.ranks_of(info["Y"])
+            assert max(O.ranks_of(info["Y"])) == rhat
+        assert np.linalg.norm(y[i] - want) <= 1e-9 * np.linalg.norm(want)
