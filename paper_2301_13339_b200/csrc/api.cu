@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -33,6 +34,19 @@ int sm_count() {
     cache[dev].store(v);
   }
   return v;
+}
+// One non-blocking side stream per device: the f and g decompositions of a
+// single-image convolution run as two chains, so the one-CTA solves of one
+// overlap the HBM passes of the other.
+cudaStream_t side_stream() {
+  static std::mutex mu;
+  static cudaStream_t cache[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!cache[dev] && cudaStreamCreateWithFlags(&cache[dev], cudaStreamNonBlocking) != cudaSuccess)
+    cache[dev] = nullptr;
+  return cache[dev];
 }
 }  // namespace qtt
 
@@ -204,6 +218,7 @@ struct DecScratch {
   double* proj;
   double* tau2;
   double* psk;
+  double* gsum;
 };
 DecScratch take_dec(Carver& cv, int d, bool rsvd = false) {
   DecScratch s{};
@@ -217,6 +232,7 @@ DecScratch take_dec(Carver& cv, int d, bool rsvd = false) {
   }
   s.proj = cv.take<double>(32 * 16);
   s.tau2 = cv.take<double>(1);
+  s.gsum = cv.take<double>(1024);
   return s;
 }
 
@@ -249,7 +265,7 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
     p.bx = s->bits[0];
     p.d = d;
     p.dl = d;
-    p.gsum = nullptr;
+    p.gsum = sc.gsum;
     p.Wa = sc.Wa; p.Wb = sc.Wb; p.part = sc.part; p.proj = sc.proj; p.tau2 = sc.tau2;
     p.cores = tt.cores + (size_t)i * d * SLOT;
     p.ranks = tt.ranks + (size_t)i * 64;
@@ -971,7 +987,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
       p.bx = shape->bits[0];
       p.d = d_;
       p.dl = d_;
-      p.gsum = nullptr;
+      p.gsum = sc.gsum;
       p.Wa = sc.Wa; p.Wb = sc.Wb; p.part = sc.part; p.proj = sc.proj; p.tau2 = sc.tau2;
       p.cores = (isf ? F.cores : G.cores) + (size_t)j * d_ * SLOT;
       p.ranks = (isf ? F.ranks : G.ranks) + (size_t)j * 64;
@@ -982,7 +998,24 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
     if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), h.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
                         "copy descriptors")))
       return r;
-    if ((r = cuda_check(launch_ttsvd(dp, nf + ng, d_, prm, st), "TT-SVD launch"))) return r;
+    cudaStream_t side = (nf + ng == 2) ? side_stream() : nullptr;
+    if (side) {
+      // f on the caller's stream, g on the side stream (fork / join events):
+      // the one-CTA solves of one chain run under the HBM passes of the other
+      cudaEvent_t fork = nullptr, join = nullptr;
+      if ((r = cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event"))) return r;
+      if ((r = cuda_check(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "event"))) return r;
+      cudaEventRecord(fork, st);
+      cudaStreamWaitEvent(side, fork, 0);
+      if ((r = cuda_check(launch_ttsvd(dp + 1, 1, d_, prm, side, 4), "TT-SVD launch"))) return r;
+      if ((r = cuda_check(launch_ttsvd(dp, 1, d_, prm, st, 4), "TT-SVD launch"))) return r;
+      cudaEventRecord(join, side);
+      if ((r = cuda_check(cudaStreamWaitEvent(st, join, 0), "join"))) return r;
+      cudaEventDestroy(fork);
+      cudaEventDestroy(join);
+    } else if ((r = cuda_check(launch_ttsvd(dp, nf + ng, d_, prm, st), "TT-SVD launch"))) {
+      return r;
+    }
   }
   prof_mark(1, st);
   // Step 3

@@ -8,9 +8,12 @@
 //       from a suffix stack of the top cores and a 7-level tree of the mid
 //       cores
 //   y_tile = [Re L, -Im L] (256 x 2r) . [Re R; Im R] (2r x 128)
-// on FP64 tensor cores (DMMA); each accumulator fragment is stored directly
-// (8 consecutive QTT indices per column = whole 32-byte sectors in both
-// layouts, streaming stores) — the pass is bound by HBM writes.
+// on FP64 tensor cores (DMMA); the accumulator fragments of each 2048-index
+// block (256 rows x 8 columns) go through a swizzled shared-memory block and
+// leave as 512-byte rows of 16-byte streaming stores (a 64 x 32 rectangle of
+// the image in the interleaved layout, 16 KB contiguous otherwise) — the pass
+// is bound by HBM writes (tools/probe/store_pattern.cu: direct fragment
+// stores 4.4 TB/s, staged 5.9-6.3 TB/s on the interleaved layout).
 #include "qtt_kernels.h"
 
 namespace qtt {
@@ -108,8 +111,26 @@ template <int R>
 struct ExSmem {
   double Rs[2 * R * RSLD];    // [Re R; Im R] (KL x 128), row-major, ld RSLD
   cplx stack[MAXD + 1][R];    // stack[k-1] = C_k ... C_d (vector of size r_{k-1})
-  cplx tree[2][NCOL * R];
+  cplx tree[2][NCOL * R];     // mid tree; reused as the 2 x 2048-double output stage
+  cplx midc[R <= 8 ? MB : 1][2 * R * R];   // cores ME+1 .. ME+MB (R <= 8: cached here)
+  int rk[MAXD + 1];           // ranks
 };
+static_assert(NCOL * 8 * sizeof(cplx) >= 2048 * sizeof(double), "stage fits a tree buffer");
+
+// Stage position of block-local QTT index q = row + 256 col (bits 0..10).
+// Interleaved: x = even bits (6), y = odd bits (5), row-major 32 x 64 with
+// the 16-byte pairs swizzled, x' = x ^ (h << 1), h = y0 | y4 << 1 | x5 << 2,
+// so the fragment stores (lanes spanning x0, y0, x1, y4, x5) hit 16 distinct
+// bank pairs per half-warp; otherwise q ^ (((q >> 9) & 3) << 2).  Both keep
+// the pairs (2m, 2m+1) adjacent for the 16-byte reads.
+__device__ __forceinline__ int stage_pos(int q, bool il) {
+  if (il) {
+    const int x = (int)compact_even((uint64_t)q), y = (int)compact_even((uint64_t)q >> 1);
+    const int h = (y & 1) | (((y >> 4) & 1) << 1) | (((x >> 5) & 1) << 2);
+    return y * 64 + (x ^ (h << 1));
+  }
+  return q ^ (((q >> 9) & 3) << 2);
+}
 
 template <int R>
 __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb* probs, ExParams P, int per_cta) {
@@ -137,11 +158,21 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       afr[mb][ks] = (col < kl) ? pr.lsplit[row + 256 * col] : 0.0;
     }
   if (tid < R) S.stack[d][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
-  uint32_t offrow[4], offcol[2];
+  for (int k = tid; k <= d; k += NT) S.rk[k] = pr.ranks[k];
+  if constexpr (R <= 8) {
+    for (int e = tid; e < MB * 2 * R * R; e += NT) {
+      const int m = e / (2 * R * R), o = e % (2 * R * R);
+      S.midc[m][o] = pr.cores[(size_t)(ME + m) * SLOT + o];   // core ME+1+m
+    }
+  }
+  const bool il = P.layout == LAYOUT_INTERLEAVED;
+  int spos[4][2];
 #pragma unroll
-  for (int mb = 0; mb < 4; ++mb) offrow[mb] = (uint32_t)qtt_offset(32 * w + 8 * mb + (lane >> 2), P.layout, P.bx);
+  for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-  for (int e = 0; e < 2; ++e) offcol[e] = (uint32_t)qtt_offset((uint64_t)(2 * (lane & 3) + e) << ME, P.layout, P.bx);
+    for (int e = 0; e < 2; ++e) spos[mb][e] = stage_pos(32 * w + 8 * mb + (lane >> 2) + 256 * (2 * (lane & 3) + e), il);
+  const uint64_t W = il ? (1ull << P.bx) : 0;
+  const bool al16 = ((uintptr_t)pr.y & 15) == 0;   // else two 8-byte stores per pair
   uint64_t prev = ~0ull;
   for (uint64_t c = c0; c < c1; ++c) {
     // ---- suffix stack over the top cores TOP0..d for the bits of c
@@ -152,7 +183,7 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
     __syncthreads();
     if (w == 0) {
       for (int k = hi; k >= TOP0; --k) {
-        const int r0 = pr.ranks[k - 1], r1 = pr.ranks[k];
+        const int r0 = S.rk[k - 1], r1 = S.rk[k];
         const int be = (int)((c >> (k - TOP0)) & 1);
         const cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
         if (lane < r0) {
@@ -170,8 +201,10 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
     int nv = 1, cur = 0;
 #pragma unroll 1
     for (int k = ME + MB; k >= ME + 1; --k) {
-      const int r0 = pr.ranks[k - 1], r1 = pr.ranks[k];
-      const cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
+      const int r0 = S.rk[k - 1], r1 = S.rk[k];
+      const cplx* core;
+      if constexpr (R <= 8) core = S.midc[k - ME - 1];
+      else core = pr.cores + (size_t)(k - 1) * SLOT;
       cplx* vout = S.tree[cur];
       for (int e = tid; e < 2 * nv * r0; e += NT) {
         const int i = e % r0, vv = e / r0;
@@ -198,15 +231,13 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       S.Rs[row * RSLD + col] = v;
     }
     __syncthreads();
-    // ---- GEMM (256 x 128) and direct stores from the fragments.  The layout
-    //      offset is additive over disjoint QTT bit fields: base (bits >= 15)
-    //      + row (bits 0..7) + column block nb (bits 11..14) + column in
-    //      block (bits 8..10), all precomputed outside the inner loop.
+    // ---- GEMM (256 x 128) in 16 blocks of 8 columns (2048 QTT indices);
+    //      each block is staged in a tree buffer (double-buffered: one barrier
+    //      per block) and written as 512-byte rows
     const uint64_t qbase = c << (ME + MB);
-    double* ybase = pr.y + qtt_offset(qbase, P.layout, P.bx);
 #pragma unroll 1
     for (int nb = 0; nb < NCOL / 8; ++nb) {
-      const uint32_t offnb = (uint32_t)qtt_offset((uint64_t)(8 * nb) << ME, P.layout, P.bx);
+      double* stg = reinterpret_cast<double*>(S.tree[nb & 1]);
       double acc[4][2];
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb) acc[mb][0] = acc[mb][1] = 0.0;
@@ -221,7 +252,26 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
 #pragma unroll
       for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) __stcs(ybase + (offrow[mb] + offcol[e] + offnb), acc[mb][e]);
+        for (int e = 0; e < 2; ++e) stg[spos[mb][e]] = acc[mb][e];
+      __syncthreads();
+      double* yb = pr.y + qtt_offset(qbase + ((uint64_t)nb << 11), P.layout, P.bx);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int pi = tid + NT * t;      // 16-byte pair in storage order
+        if (il) {
+          const int yy = pi >> 5, x = 2 * (pi & 31);
+          const int h = (yy & 1) | (((yy >> 4) & 1) << 1) | (((x >> 5) & 1) << 2);
+          const double2 v = *reinterpret_cast<const double2*>(stg + yy * 64 + (x ^ (h << 1)));
+          double* dst = yb + yy * W + x;
+          if (al16) __stcs(reinterpret_cast<double2*>(dst), v);
+          else { __stcs(dst, v.x); __stcs(dst + 1, v.y); }
+        } else {
+          const int q = 2 * pi;
+          const double2 v = *reinterpret_cast<const double2*>(stg + (q ^ (((q >> 9) & 3) << 2)));
+          if (al16) __stcs(reinterpret_cast<double2*>(yb + q), v);
+          else { __stcs(yb + q, v.x); __stcs(yb + q + 1, v.y); }
+        }
+      }
     }
   }
 }

@@ -53,7 +53,8 @@ struct DecParams {
   int kp;            // TT-RSVD sketch width k + p = rmax + p (0: plain SVD steps)
 };
 cudaError_t setup_ttsvd_kernels();
-cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st);
+cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st,
+                         int reserve = 0);
 
 // Column-sharded TT-SVD: the steps, launched one by one by the
 // host driver in api.cu, which inserts the cross-rank collectives.  `sh`

@@ -16,6 +16,9 @@
 //                     memory (and does small tensors, d <= 12, entirely).
 // Truncation: tau^2 = eps^2 ||x||^2 / (d-1) (reading Q1), rank =
 // RANK(lambda, tau^2, R_max, delta_c) on the Gram eigenvalues lambda = sigma^2.
+#include <functional>
+#include <vector>
+
 #include "qtt_dev.cuh"
 #include "qtt_kernels.h"
 
@@ -698,7 +701,13 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
     }
     return;
   }
+#ifdef QTT_STEP_TIMING
+  long long c0 = clock64();
+#endif
   eig_values<NE, NT>(S.E, rr);
+#ifdef QTT_STEP_TIMING
+  long long c1 = clock64();
+#endif
   if (tid == 0) {
     int mp = rr < (1 << (pr.d - k)) ? rr : (1 << (pr.d - k));
     S.rk = rank_choose(S.E.lam, mp, *pr.tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
@@ -706,6 +715,12 @@ __global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, 
   __syncthreads();
   const int rk = S.rk;
   const cplx* U = eig_vectors<NE, NT>(S.E, rr, rk, prm.status);
+#ifdef QTT_STEP_TIMING
+  if (tid == 0)
+    printf("step %d prob %d rr %d rk %d values %lld vectors %lld fallbacks %d tphase %lld %lld %lld %lld %lld\n", k,
+           blockIdx.y, rr, rk, c1 - c0, clock64() - c1, *prm.status, S.E.u.tr.tph[0], S.E.u.tr.tph[1],
+           S.E.u.tr.tph[2], S.E.u.tr.tph[3], S.E.u.tr.tph[4]);
+#endif
   write_core_from_U(pr, k, U, LD, rr, rk);
   for (int e = tid; e < rr * rk; e += NT) {
     int a = e % rr, r = e / rr;
@@ -875,9 +890,18 @@ __global__ void __launch_bounds__(NT) k_gram_reduce(const DecProb* sh, int nloca
   double tot = 0.0;
   for (int j = 0; j < nlocal; ++j) {
     const DecProb& pr = sh[t * nlocal + j];
-    double s = 0.0;
-    for (int b = wb; b < nblk; b += NT / 32) s += pr.part[(size_t)b * 1024 + e];
-    red[wb][lane] = s;
+    // 4 independent chains per lane keep 4 loads in flight; fixed order
+    constexpr int W = NT / 32;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int b = wb;
+    for (; b + 3 * W < nblk; b += 4 * W) {
+      s0 += pr.part[(size_t)b * 1024 + e];
+      s1 += pr.part[(size_t)(b + W) * 1024 + e];
+      s2 += pr.part[(size_t)(b + 2 * W) * 1024 + e];
+      s3 += pr.part[(size_t)(b + 3 * W) * 1024 + e];
+    }
+    for (; b < nblk; b += W) s0 += pr.part[(size_t)b * 1024 + e];
+    red[wb][lane] = (s0 + s1) + (s2 + s3);
     __syncthreads();
     if (wb == 0) {
       double u = 0.0;
@@ -912,10 +936,13 @@ __global__ void __launch_bounds__(NT) k_gather_w(const DecProb* sh, const DecPro
 // per SM of the device however many problems it carries, so batched
 // launches keep several chunks per CTA (the cp.async double buffer reaches
 // steady state) and write few per-CTA partial Grams (8 KiB each).
+// grid cap override while planning a launch with reserved slots (launch_ttsvd)
+static thread_local int t_grid_cap = 0;
 static inline int per_problem(uint64_t nchunks, int nprob) {
   const int grid_target = 4 * sm_count();
   uint64_t want = (uint64_t)((grid_target + nprob - 1) / nprob);
   if (want > (uint64_t)NBLK_MAX) want = NBLK_MAX;
+  if (t_grid_cap > 0 && want > (uint64_t)t_grid_cap) want = t_grid_cap;
   if (want > nchunks) want = nchunks;
   return want < 1 ? 1 : (int)want;
 }
@@ -936,7 +963,13 @@ cudaError_t launch_gram_reduce(const DecProb* sh, int ntens, int nlocal, int nbl
   return cudaGetLastError();
 }
 
+// The solve kernels run in one CTA per tensor: the per-CTA partial Grams are
+// summed first by k_gram_reduce (32 CTAs per tensor) into gsum.
 cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams prm, cudaStream_t st, int nsk) {
+  if (nblk > 0) {
+    launch_gram_reduce(tn, ntens, 1, nblk, st);
+    nblk = 0;
+  }
   if (narrow(prm)) k_level_solve<20><<<dim3(1, ntens), NT, smem_level_solve<20>(), st>>>(tn, nblk, prm, nsk);
   else k_level_solve<32><<<dim3(1, ntens), NT, smem_level_solve<32>(), st>>>(tn, nblk, prm, nsk);
   count_launches(1);
@@ -945,6 +978,10 @@ cudaError_t launch_level_solve(const DecProb* tn, int ntens, int nblk, DecParams
 
 cudaError_t launch_step_solve(const DecProb* tn, int ntens, int k, int nblk, DecParams prm, cudaStream_t st,
                               int nsk) {
+  if (nblk > 0) {
+    launch_gram_reduce(tn, ntens, 1, nblk, st);
+    nblk = 0;
+  }
   if (narrow(prm)) k_step_solve<20><<<dim3(1, ntens), NT, smem_step_solve<20>(), st>>>(tn, k, nblk, prm, nsk);
   else k_step_solve<32><<<dim3(1, ntens), NT, smem_step_solve<32>(), st>>>(tn, k, nblk, prm, nsk);
   count_launches(1);
@@ -1001,52 +1038,79 @@ cudaError_t setup_ttsvd_kernels() {
   return cudaSuccess;
 }
 
-// Launch the whole TT-SVD for nprob problems of equal d (device array probs).
-cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st) {
+// The TT-SVD of nprob problems of equal d as a list of launches, each tagged
+// HBM (a pass over x or W: grid over all SMs) or latency-bound (the one-CTA
+// solves and their partial-Gram reduction).
+struct TtsvdOp {
+  bool hbm;
+  std::function<void(cudaStream_t)> run;
+};
+static std::vector<TtsvdOp> ttsvd_ops(const DecProb* probs_dev, int nprob, int d, DecParams prm) {
+  std::vector<TtsvdOp> ops;
   if (d <= FIN_D) {
-    return launch_finish(probs_dev, nprob, 1, 1, prm, st);
+    ops.push_back({false, [=](cudaStream_t st) { launch_finish(probs_dev, nprob, 1, 1, prm, st); }});
+    return ops;
   }
   const int nblk = dec_nblk(d, nprob);
-  k_level_gram<<<dim3(nblk, nprob), NT, smem_level_gram(), st>>>(probs_dev, nblk, prm.status);
-  count_launches(1);
   // TT-RSVD (modification (2)): level sketches Z_5 (and Z_4) from one more pass over x
   int nsx = 0;
-  if (prm.kp > 0 && (1ull << (d - LVL_M)) > (uint64_t)prm.kp) {
-    nsx = nblk;
-    const int need4 = (16 > prm.kp) && ((1ull << (d - 4)) > (uint64_t)prm.kp);
-    k_sketch_x<<<dim3(nsx, nprob), NT, sizeof(SketchXSmem), st>>>(probs_dev, nsx, prm.kp, need4);
+  if (prm.kp > 0 && (1ull << (d - LVL_M)) > (uint64_t)prm.kp) nsx = nblk;
+  ops.push_back({true, [=](cudaStream_t st) {
+    k_level_gram<<<dim3(nblk, nprob), NT, smem_level_gram(), st>>>(probs_dev, nblk, prm.status);
     count_launches(1);
-  }
-  launch_level_solve(probs_dev, nprob, nblk, prm, st, nsx);
+    if (nsx) {
+      const int need4 = (16 > prm.kp) && ((1ull << (d - 4)) > (uint64_t)prm.kp);
+      k_sketch_x<<<dim3(nsx, nprob), NT, sizeof(SketchXSmem), st>>>(probs_dev, nsx, prm.kp, need4);
+      count_launches(1);
+    }
+  }});
+  ops.push_back({false, [=](cudaStream_t st) { launch_level_solve(probs_dev, nprob, nblk, prm, st, nsx); }});
   // K3: W_m from x, Gram for step m+1
   int k = LVL_M;
-  {
-    int nb = proj_nblk(1 << (d - k), nprob);
+  const int nb = proj_nblk(1 << (d - k), nprob);
+  ops.push_back({true, [=](cudaStream_t st) {
     k_project<true><<<dim3(nb, nprob), NT, smem_project(), st>>>(probs_dev, k, nb, 1);
     count_launches(1);
-    int src_is_a = 1;  // W_m lives in Wa
-    int prev_nb = nb;
-    ++k;
-    // steps while W_{k-1} has more than FIN_COLS columns
-    while ((1 << (d - k + 1)) > FIN_COLS) {
-      // TT-RSVD: sketch of A^{k} = reshape(W_{k-1}) when its columns exceed k + p
-      int nsk = 0;
-      if (prm.kp > 0 && (1ull << (d - k)) > (uint64_t)prm.kp) {
-        nsk = per_problem((1ull << (d - k)) / 64, nprob);
+  }});
+  int src_is_a = 1;  // W_m lives in Wa
+  int prev_nb = nb;
+  ++k;
+  // steps while W_{k-1} has more than FIN_COLS columns
+  while ((1 << (d - k + 1)) > FIN_COLS) {
+    // TT-RSVD: sketch of A^{k} = reshape(W_{k-1}) when its columns exceed k + p
+    int nsk = 0;
+    if (prm.kp > 0 && (1ull << (d - k)) > (uint64_t)prm.kp) nsk = per_problem((1ull << (d - k)) / 64, nprob);
+    ops.push_back({false, [=](cudaStream_t st) {
+      if (nsk) {
         k_sketch_w<<<dim3(nsk, nprob), NT, sizeof(SketchWSmem), st>>>(probs_dev, k - 1, nsk, src_is_a, prm.kp);
         count_launches(1);
       }
       launch_step_solve(probs_dev, nprob, k, prev_nb, prm, st, nsk);
-      int nb2 = proj_nblk(1 << (d - k), nprob);
+    }});
+    const int nb2 = proj_nblk(1 << (d - k), nprob);
+    ops.push_back({true, [=](cudaStream_t st) {
       k_project<false><<<dim3(nb2, nprob), NT, smem_project(), st>>>(probs_dev, k, nb2, src_is_a);
       count_launches(1);
-      src_is_a ^= 1;
-      prev_nb = nb2;
-      ++k;
-    }
-    launch_finish(probs_dev, nprob, k, src_is_a, prm, st);
+    }});
+    src_is_a ^= 1;
+    prev_nb = nb2;
+    ++k;
   }
+  ops.push_back({false, [=](cudaStream_t st) { launch_finish(probs_dev, nprob, k, src_is_a, prm, st); }});
+  return ops;
+}
+
+// Launch the whole TT-SVD for nprob problems of equal d (device array probs).
+// reserve > 0: the HBM passes leave `reserve` CTA slots free (2 CTAs per SM
+// otherwise), so a solve CTA of a concurrent chain on another stream becomes
+// resident at once instead of after the whole pass (see qtt_conv_full).
+cudaError_t launch_ttsvd(const DecProb* probs_dev, int nprob, int d, DecParams prm, cudaStream_t st, int reserve) {
+  if (reserve > 0) t_grid_cap = 2 * sm_count() - reserve;
+  std::vector<TtsvdOp> ops = ttsvd_ops(probs_dev, nprob, d, prm);
+  t_grid_cap = 0;
+  for (const TtsvdOp& op : ops) op.run(st);
   return cudaGetLastError();
 }
+
 
 }  // namespace qtt

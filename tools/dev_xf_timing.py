@@ -2,7 +2,7 @@
 import sys, ctypes, numpy as np, torch
 sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
 from paper_2301_13339_b200 import synth, qtt as Q
-Q.LIB_PATH = '/root/repo/build/libqtt_timing.so'
+import os; Q.LIB_PATH = os.environ.get('QTT_LIB', '/root/repo/build_tmp/libqtt_xf.so')
 from gpu_util import *
 def run(x, label, inverse=False):
     tt = gpu_decompose(x, "interleaved", 1e-3, 10)
