@@ -73,7 +73,8 @@ typedef struct {
 } qtt_shape;
 
 /* Truncation policy: eps >= 0, 1 <= rmax <= 16, cluster_tol >= 0.
- * Decomposition caps use rmax (R_max <= 10); transform/rounding caps Rhat
+ * Decomposition caps use rmax (R_max <= 16; <= 10 with a communicator or
+ * for the sharded workspace query); transform/rounding caps Rhat
  * (<= 16; the paper's Rhat_max = 15).  Rhat <= 8 runs the
  * one-CTA Hadamard rounding, 9..16 the multi-CTA one (Kronecker ranks of
  * F (.) G up to 160 resp. 256).

@@ -333,11 +333,12 @@ qtt_status run_expand(const cplx* cores, const int* ranks, int nt, int d, double
 // Step 3 on handles' storage: F (nf tensors), G (ng = 1 or nf) -> Y (nf)
 qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, const int* gr, int ng,
                         const qtt_shape* s, const qtt_trunc* fft, const long long* shift, double scale,
-                        TTAlloc Y, Carver& cv, int* status, cudaStream_t st) {
+                        TTAlloc Y, Carver& cv, int* status, cudaStream_t st, int in_rcap) {
   const int d = shape_d(s);
   // Rhat <= RH_MAX: one-CTA rounding; above: the multi-CTA variant (Kronecker ranks <= 256)
   const bool big = fft->rmax > RH_MAX;
-  const int rs = fft->rmax > RS_XF ? RS_BIG : RS_XF;
+  // transform variant: compact cores in shared memory while every rank fits RS_XF
+  const int rs = (fft->rmax > RS_XF || in_rcap > RS_XF) ? RS_BIG : RS_XF;
   TTAlloc Fh = take_tt(cv, nf, d);
   TTAlloc Gh = take_tt(cv, ng, d);
   TTAlloc Z = take_tt(cv, nf, d);
@@ -715,7 +716,7 @@ size_t ws_sharded(const qtt_shape* shape, const qtt_trunc* fft, int P, int nloca
   ShardDec D;
   plan_sharded_dec(cv, shape, g, P, nlocal, 0, 2, xs, tt, D);
   run_convolve(tt[0].cores, tt[0].ranks, 1, tt[1].cores, tt[1].ranks, 1, shape, fft, nullptr, 1.0, Y, cv, nullptr,
-               nullptr);
+               nullptr, RS_GATHER);
   ShardEx E;
   plan_sharded_expand(cv, Y.cores, Y.ranks, g, nlocal, 0, nullptr, E);
   return cv.off + 4096;
@@ -754,7 +755,8 @@ const char* qtt_build_info(void) {
 }
 
 size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const qtt_trunc* fft, int nranks) {
-  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec", true) || check_trunc(fft, RH_BIG, "fft") || nranks < 1)
+  if (check_shape(shape) || check_trunc(dec, nranks > 1 ? RS_GATHER : RC, "dec", true) ||
+      check_trunc(fft, RH_BIG, "fft") || nranks < 1)
     return 0;
   if (nranks > 1 && dec->rule == QTT_RULE_RSVD) return 0;
   if (nranks > 1) return ws_sharded(shape, fft, nranks, 1);
@@ -767,7 +769,8 @@ size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const q
   // (dry runs of the same carving sequence qtt_conv_full performs)
   for (int i = 0; i < nf + ng; ++i) take_dec(cv, d, dec->rule == QTT_RULE_RSVD);
   cv.take<DecProb>(nf + ng);
-  run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, nullptr, 1.0, Y, cv, nullptr, nullptr);
+  run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, nullptr, 1.0, Y, cv, nullptr, nullptr,
+               dec->rmax);
   run_expand(Y.cores, Y.ranks, nf, d, nullptr, 0, shape, 0, cv, nullptr);
   const size_t one = ws_sharded(shape, fft, 1, 1);   // a 1-rank communicator takes the sharded path
   return cv.off + 4096 > one ? cv.off + 4096 : one;
@@ -776,7 +779,7 @@ size_t qtt_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const q
 size_t qtt_comm_workspace_bytes(const qtt_shape* shape, const qtt_trunc* dec, const qtt_trunc* fft,
                                 qtt_comm_t comm) {
   if (!comm) return qtt_workspace_bytes(shape, dec, fft, 1);
-  if (check_shape(shape) || check_trunc(dec, RS_XF, "dec") || check_trunc(fft, RH_BIG, "fft")) return 0;
+  if (check_shape(shape) || check_trunc(dec, RS_GATHER, "dec") || check_trunc(fft, RH_BIG, "fft")) return 0;
   return ws_sharded(shape, fft, comm->nshards, comm->nlocal);
 }
 
@@ -875,7 +878,8 @@ qtt_status qtt_convolve(qtt_tt_t f, qtt_tt_t g, const qtt_trunc* fft, const long
   if ((r = check_trunc(fft, RH_BIG, "fft"))) return r;
   if (f->d != g->d) return fail(QTT_EINVAL, "f and g have different d");
   if (g->nt != 1 && g->nt != f->nt) return fail(QTT_EINVAL, "g must hold 1 tensor or as many as f");
-  if (f->rcap > RS_XF || g->rcap > RS_XF) return fail(QTT_EINVAL, "input ranks may exceed %d", RS_XF);
+  if (f->rcap > RS_BIG || g->rcap > RS_BIG) return fail(QTT_EINVAL, "input ranks may exceed %d", RS_BIG);
+  const int in_rcap = f->rcap > g->rcap ? f->rcap : g->rcap;
   cudaError_t ce;
   if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
   const int d = f->d;
@@ -883,12 +887,12 @@ qtt_status qtt_convolve(qtt_tt_t f, qtt_tt_t g, const qtt_trunc* fft, const long
   Carver dry(nullptr);
   TTAlloc Y = take_tt(dry, f->nt, d);
   run_convolve(f->cores, f->ranks, f->nt, g->cores, g->ranks, g->nt, &f->shape, fft, shift, scale, Y, dry,
-               nullptr, st);
+               nullptr, st, in_rcap);
   if ((r = check_ws(dry, ws, ws_bytes))) return r;
   Carver cv(ws);
   Y = take_tt(cv, f->nt, d);
   if ((r = run_convolve(f->cores, f->ranks, f->nt, g->cores, g->ranks, g->nt, &f->shape, fft, shift, scale, Y,
-                        cv, f->status, st)))
+                        cv, f->status, st, in_rcap)))
     return r;
   *out = new_handle(&f->shape, f->nt, fft->rmax, Y, f->status, st);
   return *out ? QTT_OK : fail(QTT_ENOMEM, "host allocation failed");
@@ -936,7 +940,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
                          void* stream, qtt_comm_t comm, qtt_report* rep_host) {
   qtt_status r;
   if ((r = check_shape(shape))) return r;
-  if ((r = check_trunc(dec, RS_XF, "dec", !comm))) return r;
+  if ((r = check_trunc(dec, comm ? RS_GATHER : RC, "dec", !comm))) return r;
   if ((r = check_trunc(fft, RH_BIG, "fft"))) return r;
   if (!f || !g || !y) return fail(QTT_EINVAL, "f / g / y is NULL");
   ShardGeom geo{};
@@ -1019,7 +1023,8 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   }
   prof_mark(1, st);
   // Step 3
-  if ((r = run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, shift, scale, Y, cv, status, st)))
+  if ((r = run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, shift, scale, Y, cv, status, st,
+                        dec->rmax)))
     return r;
   // Step 4
   if (comm) {

@@ -60,10 +60,17 @@ def test_workspace_bytes_validation(L):
         (Q.shape(2, [9, 9], "1d"), dec, fft),                     # layout mismatch
         (Q.shape(2, [9, 9], "interleaved"), Q.trunc(-1.0, 10), fft),
         (Q.shape(2, [9, 9], "interleaved"), Q.trunc(1e-3, 0), fft),
-        (Q.shape(2, [9, 9], "interleaved"), dec, Q.trunc(1e-3, 9)),   # Rhat > 8
+        (Q.shape(2, [9, 9], "interleaved"), dec, Q.trunc(1e-3, 17)),  # Rhat > 16
+        (Q.shape(2, [9, 9], "interleaved"), Q.trunc(1e-3, 17), fft),  # R_max > 16
     ]
     for s, a, b in bad:
         assert L.qtt_workspace_bytes(ctypes.byref(s), ctypes.byref(a), ctypes.byref(b), 1) == 0
+    # the paper's caps (10, 15) and (16, 16) are valid; sharded plans keep R_max <= 10
+    shp = Q.shape(2, [9, 9], "interleaved")
+    for a, b in ((dec, Q.trunc(1e-3, 15)), (Q.trunc(1e-3, 16), Q.trunc(1e-3, 16))):
+        assert L.qtt_workspace_bytes(ctypes.byref(shp), ctypes.byref(a), ctypes.byref(b), 1) > 0
+    big = Q.trunc(1e-3, 16)
+    assert L.qtt_workspace_bytes(ctypes.byref(shp), ctypes.byref(big), ctypes.byref(fft), 2) == 0
 
 
 def test_invalid_arguments_fail_before_any_device_work(L):

@@ -104,3 +104,29 @@ def test_conv_big_rounding_caps(rhat, layout):
             assert rep["ranks_out"] == O.ranks_of(info["Y"])
             assert max(O.ranks_of(info["Y"])) == rhat
         assert np.linalg.norm(y[i] - want) <= 1e-9 * np.linalg.norm(want)
+
+
+@pytest.mark.parametrize("layout", ["interleaved", "1d"])
+def test_conv_caps_16_16(layout):
+    """N4's larger cap set (R_max, Rhat_max) = (16, 16): TT-SVD at rank 16,
+    transforms on workspace-resident cores, the multi-CTA rounding."""
+    if layout == "1d":
+        f = synth.random_signal((1 << 14,), 91, kind="smooth") + 0.05 * synth.random_signal((1 << 14,), 92)
+        g = synth.random_signal((1 << 14,), 93, kind="smooth")
+        shift = (1 << 13, 0)
+    else:
+        f = synth.random_signal((128, 128), 94, kind="smooth") + 0.05 * synth.random_signal((128, 128), 95)
+        g = synth.random_signal((128, 128), 96, kind="smooth")
+        shift = (64, 64)
+    # eps = 1e-5: at 1e-6 the kept components reach ~3e-7 sigma_1, where the
+    # Gram truncation's ~eps_mach / s error per component (DESIGN.md 5.3)
+    # sums to ~3e-9 over the chain (probe: the oracle itself moves 5e-15)
+    dec, fft = (1e-5, 16, 1e-10), (1e-5, 16, 1e-10)
+    y, rep = gpu_conv_full(f, g, layout, dec, fft, shift, 0.25)
+    want, info = O.conv_pipeline(f, g, layout, dec, fft, shift, 0.25, return_info=True)
+    assert rep["status_bits"] & 3 == 0
+    assert max(O.ranks_of(info["F"])) == 16
+    assert rep["ranks_f"] == O.ranks_of(info["F"])
+    assert rep["ranks_g"] == O.ranks_of(info["G"])
+    assert rep["ranks_out"] == O.ranks_of(info["Y"])
+    assert np.linalg.norm(y - want) <= 1e-9 * np.linalg.norm(want)
