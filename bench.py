@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-fft-comparator", action="store_true")
     ap.add_argument("--ref-step-seconds", type=float, default=None,
                     help="--impl reference: CPU seconds per step (default: ~60 s over the whole run)")
+    ap.add_argument("--caps-sweep", action="store_true",
+                    help="N4 quality sweep: E2 vs the clean convolution at caps (10,8), (10,15), (16,16)")
     ap.add_argument("--rhat", type=int, default=None,
                     help="override the QTT-FFT / rounding cap Rhat_max (default 8, reading Q4; paper 15)")
     return ap.parse_args()
@@ -364,6 +366,37 @@ def run_ours(a):
         fftc = fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, a.steps, dev,
                               clean=np.ascontiguousarray(clean0))
 
+    # N4 quality sweep: E2 of the QTT result against the
+    # convolution of the CLEAN signal at the caps (10, 8) (default, reading Q4),
+    # (10, 15) (the paper's) and (16, 16), with each one's time (--caps-sweep)
+    caps_sweep = []
+    if a.caps_sweep and mode != "sharded":
+        n1 = 1 << p["b"]
+        clean0 = np.ascontiguousarray(synth.signal(cfg, index=rank * batch if mode == "batch" else rank,
+                                                   noisy=False))
+        gsh = torch.roll(g_d.view((n1,) * D), shifts=tuple(-s for s in p["shift"][::-1]), dims=tuple(range(D)))
+        c = torch.from_numpy(clean0).to(dev).view((n1,) * D)
+        ref = torch.fft.irfftn(torch.fft.rfftn(c, dim=tuple(range(D))) * torch.fft.rfftn(gsh, dim=tuple(range(D))),
+                               s=(n1,) * D, dim=tuple(range(D))) * p["scale"]
+        for rm, rh in ((10, 8), (10, 15), (16, 16)):
+            d3 = Q.trunc(eps, rm, p["cluster_tol"])
+            f3 = Q.trunc(eps, rh, p["cluster_tol"])
+            nb3 = Q.qtt_workspace_bytes(shp, d3, f3)
+            ws3 = ws if nb3 <= nb else torch.empty(nb3 + 256, dtype=torch.uint8, device=dev)
+
+            def step3(d3=d3, f3=f3, ws3=ws3, nb3=nb3):
+                Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, d3, f3, p["shift"],
+                                p["scale"], ws3.data_ptr(), nb3, sp)
+            step3()
+            ms3 = timed(step3, 2)
+            r3 = Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, d3, f3, p["shift"],
+                                 p["scale"], ws3.data_ptr(), nb3, sp, report=True)
+            torch.cuda.synchronize(dev)
+            e2 = float(torch.linalg.vector_norm(y_d[:n1 ** D].view((n1,) * D) - ref) / torch.linalg.vector_norm(ref))
+            caps_sweep.append({"caps": [rm, rh], "ms_per_step": ms3 / 2, "e2_vs_clean_conv": e2,
+                               "max_rank_f": max(r3["ranks_f"]), "max_rank_out": max(r3["ranks_out"])})
+            del ws3
+
     # BASELINE's eps sweeps (C3: {1e-2, 1e-4}, C5: {1e-1, 1e-2, 1e-3}): the other
     # listed eps on the same inputs, same timing (the headline uses the first)
     eps_sweep = []
@@ -470,6 +503,8 @@ def run_ours(a):
         line["fft_comparator"] = fftc
     if eps_sweep:
         line["eps_sweep"] = eps_sweep
+    if caps_sweep:
+        line["caps_sweep"] = caps_sweep
     # the small-core chain is a serial sequence of truncations (latency-bound):
     # forward transforms (F and G concurrently), rounding, inverse transform
     cuts = d * (d - 1) // 2

@@ -111,8 +111,14 @@ template <int R>
 struct ExSmem {
   double Rs[2 * R * RSLD];    // [Re R; Im R] (KL x 128), row-major, ld RSLD
   cplx stack[MAXD + 1][R];    // stack[k-1] = C_k ... C_d (vector of size r_{k-1})
-  cplx tree[2][NCOL * R];     // mid tree; reused as the 2 x 2048-double output stage
-  cplx midc[R <= 8 ? MB : 1][2 * R * R];   // cores ME+1 .. ME+MB (R <= 8: cached here)
+  cplx tree[2][NCOL * R];     // mid tree (R > 8); the 2 x 2048-double output stage
+  // R <= 8: the 7 mid cores as three products computed once per CTA,
+  // P_low[b9 b10 b11] = C_9 C_10 C_11, Q_a[b12 b13] = C_12 C_13 and
+  // Q_b[b14 b15] = C_14 C_15 (column (b9..b15) of R = P_low Q_a Q_b s)
+  cplx qa[R <= 8 ? 4 : 1][R * R];
+  cplx qb[R <= 8 ? 4 : 1][R * R];
+  cplx plow[R <= 8 ? R * R : 1][8];       // [i + R j][lb]: lanes of consecutive columns read consecutive lb
+  cplx ut[R <= 8 ? 2 : 1][16 * R];
   int rk[MAXD + 1];           // ranks
 };
 static_assert(NCOL * 8 * sizeof(cplx) >= 2048 * sizeof(double), "stage fits a tree buffer");
@@ -160,10 +166,39 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
   if (tid < R) S.stack[d][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
   for (int k = tid; k <= d; k += NT) S.rk[k] = pr.ranks[k];
   if constexpr (R <= 8) {
-    for (int e = tid; e < MB * 2 * R * R; e += NT) {
-      const int m = e / (2 * R * R), o = e % (2 * R * R);
-      S.midc[m][o] = pr.cores[(size_t)(ME + m) * SLOT + o];   // core ME+1+m
+    // Q_a[ha] (r_11 x r_13) = C_12[b12] C_13[b13]; Q_b[hh] (r_13 x r_15) = C_14[b14] C_15[b15]
+    for (int e = tid; e < 2 * 4 * R * R; e += NT) {
+      const int which = e / (4 * R * R), o = e % (4 * R * R);
+      const int h = o / (R * R), i = (o % (R * R)) % R, j = (o % (R * R)) / R;
+      const int k0 = which == 0 ? 12 : 14;                    // first core of the pair
+      const int ra = pr.ranks[k0 - 1], rm = pr.ranks[k0], rb = pr.ranks[k0 + 1];
+      cplx acc = czero();
+      if (i < ra && j < rb) {
+        const cplx* c0 = pr.cores + (size_t)(k0 - 1) * SLOT;
+        const cplx* c1 = pr.cores + (size_t)k0 * SLOT;
+        const int b0 = h & 1, b1 = h >> 1;
+        for (int a = 0; a < rm; ++a) acc = cfma(c0[i + ra * b0 + 2 * ra * a], c1[a + rm * b1 + 2 * rm * j], acc);
+      }
+      (which == 0 ? S.qa : S.qb)[h][i + R * j] = acc;
     }
+    // P_low[lb] (r_8 x r_11) = C_9[b9] C_10[b10] C_11[b11], lb = b9 + 2 b10 + 4 b11
+    const int q8 = pr.ranks[8], q9 = pr.ranks[9], q10 = pr.ranks[10], q11 = pr.ranks[11];
+    const cplx* c9 = pr.cores + (size_t)8 * SLOT;
+    const cplx* c10 = pr.cores + (size_t)9 * SLOT;
+    const cplx* c11 = pr.cores + (size_t)10 * SLOT;
+    for (int e = tid; e < 8 * q8 * q11; e += NT) {
+      const int i = e % q8, j = (e / q8) % q11, lb = e / (q8 * q11);
+      const int b0 = lb & 1, b1 = (lb >> 1) & 1, b2 = lb >> 2;
+      cplx acc = czero();
+      for (int b = 0; b < q10; ++b) {
+        cplx t = czero();
+        for (int a = 0; a < q9; ++a) t = cfma(c9[i + q8 * b0 + 2 * q8 * a], c10[a + q9 * b1 + 2 * q9 * b], t);
+        acc = cfma(t, c11[b + q10 * b2 + 2 * q10 * j], acc);
+      }
+      S.plow[i + R * j][lb] = acc;
+    }
+    // Rs rows 2 r_8 .. kl-1 stay zero
+    for (int e = tid; e < (kl - 2 * r8) * NCOL; e += NT) S.Rs[(2 * r8 + e / NCOL) * RSLD + e % NCOL] = 0.0;
   }
   const bool il = P.layout == LAYOUT_INTERLEAVED;
   int spos[4][2];
@@ -195,6 +230,59 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       }
     }
     prev = c;
+    if constexpr (R <= 8) {
+      // ---- warp 0: v[hh] = Q_b[hh] s (s = C_16 .. C_d, size r_15), then
+      //      u[hb] = Q_a[hb & 3] v[hb >> 2] (16 vectors of size r_11,
+      //      hb = b12 + 2 b13 + 4 b14 + 8 b15); then all threads:
+      //      R[:, col] = P_low[col & 7] u[col >> 3]
+      if (w == 0) {
+        const cplx* sv = S.stack[TOP0 - 1];
+        const int r11 = S.rk[ME + 3], r13 = S.rk[ME + 5], r15 = S.rk[ME + 7];
+        if (lane < 4 * r13) {
+          const int i = lane % r13, hh = lane / r13;
+          cplx s0 = czero(), s1 = czero();
+#pragma unroll
+          for (int j = 0; j < R; j += 2) {
+            if (j < r15) s0 = cfma(S.qb[hh][i + R * j], sv[j], s0);
+            if (j + 1 < r15) s1 = cfma(S.qb[hh][i + R * (j + 1)], sv[j + 1], s1);
+          }
+          S.ut[0][hh * R + i] = cadd(s0, s1);
+        }
+        __syncwarp();
+        for (int e = lane; e < 16 * r11; e += 32) {
+          const int i = e % r11, hb = e / r11;
+          const cplx* vv = S.ut[0] + (hb >> 2) * R;
+          const cplx* qa = S.qa[hb & 3];
+          cplx s0 = czero(), s1 = czero();
+#pragma unroll
+          for (int j = 0; j < R; j += 2) {
+            if (j < r13) s0 = cfma(qa[i + R * j], vv[j], s0);
+            if (j + 1 < r13) s1 = cfma(qa[i + R * (j + 1)], vv[j + 1], s1);
+          }
+          S.ut[1][hb * R + i] = cadd(s0, s1);
+        }
+      }
+      __syncthreads();
+      {
+        const cplx* u = S.ut[1];
+        const int r11 = S.rk[ME + 3];
+        for (int e = tid; e < NCOL * r8; e += NT) {
+          const int col = e % NCOL, i = e / NCOL;
+          const int lb = col & 7;
+          const cplx* uv = u + (col >> 3) * R;
+          cplx s0 = czero(), s1 = czero();
+#pragma unroll
+          for (int j = 0; j < R; j += 2) {
+            if (j < r11) s0 = cfma(S.plow[i + R * j][lb], uv[j], s0);
+            if (j + 1 < r11) s1 = cfma(S.plow[i + R * (j + 1)][lb], uv[j + 1], s1);
+          }
+          const cplx v = cadd(s0, s1);
+          S.Rs[i * RSLD + col] = v.x;
+          S.Rs[(r8 + i) * RSLD + col] = v.y;
+        }
+      }
+      __syncthreads();
+    } else {
     __syncthreads();
     // ---- mid tree over cores ME+MB .. ME+1 -> 64 vectors of size r_8
     const cplx* vin = S.stack[TOP0 - 1];
@@ -202,9 +290,7 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
 #pragma unroll 1
     for (int k = ME + MB; k >= ME + 1; --k) {
       const int r0 = S.rk[k - 1], r1 = S.rk[k];
-      const cplx* core;
-      if constexpr (R <= 8) core = S.midc[k - ME - 1];
-      else core = pr.cores + (size_t)(k - 1) * SLOT;
+      const cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
       cplx* vout = S.tree[cur];
       for (int e = tid; e < 2 * nv * r0; e += NT) {
         const int i = e % r0, vv = e / r0;
@@ -231,6 +317,7 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       S.Rs[row * RSLD + col] = v;
     }
     __syncthreads();
+    }
     // ---- GEMM (256 x 128) in 16 blocks of 8 columns (2048 QTT indices);
     //      each block is staged in a tree buffer (double-buffered: one barrier
     //      per block) and written as 512-byte rows
