@@ -166,7 +166,8 @@ struct TridSmem {
   cplx colx[32];             // next reflector column (rows below the diagonal)
   cplx colc[32];             // the column after it
   cplx ypart[4][32];         // per-warp partial A x
-  double red4[4];            // the four reduced sums of a reflector
+  cplx qpart[4][32];         // per-Q-warp partial Q v
+  double red8[4][2];         // per-warp reduced sums of a reflector
   cplx ph[NMAX];             // D = diag(ph)
   double tau[NMAX];
   double dg[NMAX];           // diag of T (normalised)
@@ -300,7 +301,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #else
 #define TS_MARK(q)
 #endif
-  static_assert(NT >= 160, "trid_values needs warps 0-3 (reduction) and 4 (Q)");
+  static_assert(NT >= 256, "trid_values needs warps 0-3 (reduction) and 4-7 (Q)");
   if (wp < 4) {
     // Warps 0-3 (one per SM sub-partition, so the FP64 pipes of all four
     // are used): lane i = row i, warp w owns columns j = w + 4t of the
@@ -335,6 +336,12 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       cplx xi = live ? S.colx[ri] : czero();
       const cplx ci = live ? S.colc[ri] : czero();
       const double a0 = S.colc[k + 1].x;
+      // ---- one exchange per step: each warp reduces Re(x^H y_w) of its
+      //      partial y_w = A[:, own columns] x_own together with one of |x|^2,
+      //      Re(x^H c), Im(x^H c) (x^H c = x^H A e_{k+1} is NOT replaced by
+      //      conj((A x)_{k+1}): the Gram matrices are Hermitian only to
+      //      rounding, and when x is tiny against ||A|| that asymmetry is of the
+      //      order of x itself); y_w and the sums meet at one barrier
       {
         cplx acc = czero();
 #pragma unroll
@@ -343,32 +350,30 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
           if (j > k && j < n) acc = cfma(a[t], S.colx[j], acc);   // x_j = 0 elsewhere (warp-uniform test)
         }
         S.ypart[wp][i] = acc;
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      const cplx yi = cadd(cadd(S.ypart[0][i], S.ypart[1][i]), cadd(S.ypart[2][i], S.ypart[3][i]));
-      TS_MARK(0)
-      // ---- reflector (identical in every warp)
-      // |x|^2, Re(x^H A x) and x^H c = x^H A e_{k+1}, reduced together.  x^H c
-      // is NOT replaced by conj((A x)_{k+1}): the Gram matrices are Hermitian
-      // only to rounding, and when x is tiny against ||A|| that asymmetry is
-      // of the order of x itself (the value used is the one p = tau A v,
-      // K = tau/2 Re(v^H p) would produce).
-      //      (warp w reduces the w-th of the four sums; exchanged via smem)
-      {
-        double rv = wp == 0 ? cabs2(xi)
-                  : wp == 1 ? xi.x * yi.x + xi.y * yi.y
-                  : wp == 2 ? xi.x * ci.x + xi.y * ci.y
-                            : xi.x * ci.y - xi.y * ci.x;
+        double r1 = xi.x * acc.x + xi.y * acc.y;
+        double r2 = wp == 0 ? cabs2(xi)
+                  : wp == 1 ? xi.x * ci.x + xi.y * ci.y
+                  : wp == 2 ? xi.x * ci.y - xi.y * ci.x
+                            : 0.0;
 #pragma unroll
-        for (int o = (NMAX <= 16 ? 8 : 16); o > 0; o >>= 1) rv += __shfl_xor_sync(0xffffffffu, rv, o);
-        if (i == 0) S.red4[wp] = rv;
+        for (int o = (NMAX <= 16 ? 8 : 16); o > 0; o >>= 1) {
+          r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+          r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        }
+        if (i == 0) {
+          S.red8[wp][0] = r1;
+          S.red8[wp][1] = r2;
+        }
       }
       const double x0r = __shfl_sync(0xffffffffu, xi.x, k + 1), x0i = __shfl_sync(0xffffffffu, xi.y, k + 1);
-      const double y0r = __shfl_sync(0xffffffffu, yi.x, k + 1), y0i = __shfl_sync(0xffffffffu, yi.y, k + 1);
       asm volatile("bar.sync 1, 128;" ::: "memory");
+      TS_MARK(0)
+      const cplx yi = cadd(cadd(S.ypart[0][i], S.ypart[1][i]), cadd(S.ypart[2][i], S.ypart[3][i]));
+      const cplx y0 = cadd(cadd(S.ypart[0][k + 1], S.ypart[1][k + 1]), cadd(S.ypart[2][k + 1], S.ypart[3][k + 1]));
+      const double y0r = y0.x, y0i = y0.y;
       TS_MARK(1)
-      const double s2 = S.red4[0], xAx = S.red4[1];
-      const cplx xc = cmk(S.red4[2], S.red4[3]);
+      const double s2 = S.red8[0][1], xAx = (S.red8[0][0] + S.red8[1][0]) + (S.red8[2][0] + S.red8[3][0]);
+      const cplx xc = cmk(S.red8[1][1], S.red8[2][1]);
       const double x02 = x0r * x0r + x0i * x0i;
       // reflect when the column is above 1e-30 ||A|| (below that it is
       // treated as reduced); the phase of x0 is needed whenever |x0|^2 is a
@@ -414,7 +419,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
         }
       }
       // end of step: warps 0-3 and the Q warp (160 threads)
-      asm volatile("bar.sync 2, 160;" ::: "memory");
+      asm volatile("bar.sync 2, 256;" ::: "memory");
       TS_MARK(3)
     }
     // ---- T: dg_i = A_ii, alpha_{n-2} = A_{n-1,n-2}; D = diag(ph) with
@@ -450,28 +455,41 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       for (int q = 0; q < 4; ++q) S.tstep[q] = ts[q];
     if (tid == 0) S.tph[4] = 0;
 #endif
-  } else if (wp == 4) {
-    // Q_{k+1} = Q_k H_k = Q_k - tau (Q_k v) v^H, lane = row of Q; reflector
-    // k is read after the end-of-step barrier of step k (one step behind)
-    const int i = lane;
-    if (i < n)
-      for (int j = 0; j < n; ++j) Qm[i + LD * j] = cmk(i == j ? 1.0 : 0.0, 0.0);
+  } else if (wp < 8) {
+    // Q_{k+1} = Q_k H_k = Q_k - tau (Q_k v) v^H by warps 4-7 (one per
+    // sub-partition, so the FP64 work is spread like the reduction's): lane =
+    // row of Q, warp 4+m holds the columns j = m + 4t in registers; the
+    // partial dots (Q v)_i are summed over the four warps through smem (named
+    // barrier 3).  Reflector k is read after the end-of-step barrier of step
+    // k (one step behind).
+    constexpr int TC = (NMAX + 3) / 4;
+    const int m = wp - 4, i = lane;
+    cplx q[TC];
+#pragma unroll
+    for (int t = 0; t < TC; ++t) q[t] = cmk((m + 4 * t == i) ? 1.0 : 0.0, 0.0);
     for (int k = 0; k + 2 < n; ++k) {
-      asm volatile("bar.sync 2, 160;" ::: "memory");
+      asm volatile("bar.sync 2, 256;" ::: "memory");
       const double tau = S.tau[k];
-      if (tau != 0.0 && i < n) {
-        cplx q0 = czero(), q1 = czero();
-        int j = k + 1;
-        for (; j + 1 < n; j += 2) {
-          q0 = cfma(Qm[i + LD * j], S.hv[j + LD * k], q0);
-          q1 = cfma(Qm[i + LD * (j + 1)], S.hv[j + 1 + LD * k], q1);
-        }
-        if (j < n) q0 = cfma(Qm[i + LD * j], S.hv[j + LD * k], q0);
-        const cplx sq = cscale(cadd(q0, q1), tau);
-        for (int jj = k + 1; jj < n; ++jj) {
-          cplx* q = &Qm[i + LD * jj];
-          *q = csub(*q, cmul(sq, cconj(S.hv[jj + LD * k])));
-        }
+      cplx acc = czero();
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        const int j = m + 4 * t;
+        if (j > k && j < n) acc = cfma(q[t], S.hv[j + LD * k], acc);   // warp-uniform test
+      }
+      S.qpart[m][i] = acc;
+      asm volatile("bar.sync 3, 128;" ::: "memory");
+      const cplx sq = cscale(cadd(cadd(S.qpart[0][i], S.qpart[1][i]), cadd(S.qpart[2][i], S.qpart[3][i])), tau);
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        const int j = m + 4 * t;
+        if (j > k && j < n) q[t] = csub(q[t], cmul(sq, cconj(S.hv[j + LD * k])));
+      }
+    }
+    if (i < n) {
+#pragma unroll
+      for (int t = 0; t < TC; ++t) {
+        const int j = m + 4 * t;
+        if (j < n) Qm[i + LD * j] = q[t];
       }
     }
   }
