@@ -9,7 +9,7 @@ namespace qtt {
 static constexpr int NT = 256;
 
 template <int NMAX>
-__global__ void __launch_bounds__(NT) k_debug_eigh(const cplx* A, int n, double* lam, cplx* U, int* sweeps,
+__global__ void __launch_bounds__(NT, 1) k_debug_eigh(const cplx* A, int n, double* lam, cplx* U, int* sweeps,
                                                    int reps, int mode) {
   extern __shared__ __align__(16) unsigned char smraw[];
   EigSmem<NMAX>& E = *reinterpret_cast<EigSmem<NMAX>*>(smraw);

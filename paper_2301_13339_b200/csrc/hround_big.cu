@@ -142,7 +142,7 @@ struct HrbSolveSmem {
 };
 
 // K = T E^H, eigenpairs, RANK, core c, Sm = U_r^H E.  One CTA per problem.
-__global__ void __launch_bounds__(NT) k_hrb_solve(const HrBigProb* probs, int c, int d, HrParams P) {
+__global__ void __launch_bounds__(NT, 1) k_hrb_solve(const HrBigProb* probs, int c, int d, HrParams P) {
   const HrBigProb& p = probs[blockIdx.x];
   extern __shared__ __align__(16) unsigned char smraw[];
   HrbSolveSmem& S = *reinterpret_cast<HrbSolveSmem*>(smraw);

@@ -96,7 +96,7 @@ __device__ void build_doubled(SM& S, const cplx* c, const XfParams& P, int q, in
 }
 
 template <int RSV>
-__global__ void __launch_bounds__(NT) k_transform(const XfProb* probs, XfParams P) {
+__global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfParams P) {
   const XfProb& pr = probs[blockIdx.x];
   extern __shared__ __align__(16) unsigned char smraw[];
   XfSmem<RSV>& S = *reinterpret_cast<XfSmem<RSV>*>(smraw);

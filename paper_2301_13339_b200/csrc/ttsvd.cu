@@ -450,7 +450,7 @@ struct LevelSolveSmem {
 };
 
 template <int NE>
-__global__ void __launch_bounds__(NT) k_level_solve(const DecProb* probs, int nblk, DecParams prm, int nsk) {
+__global__ void __launch_bounds__(NT, 1) k_level_solve(const DecProb* probs, int nblk, DecParams prm, int nsk) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
   LevelSolveSmem<NE>& S = *reinterpret_cast<LevelSolveSmem<NE>*>(smraw);
@@ -674,7 +674,7 @@ struct StepSolveSmem {
 };
 
 template <int NE>
-__global__ void __launch_bounds__(NT) k_step_solve(const DecProb* probs, int k, int nblk, DecParams prm, int nsk) {
+__global__ void __launch_bounds__(NT, 1) k_step_solve(const DecProb* probs, int k, int nblk, DecParams prm, int nsk) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
   StepSolveSmem<NE>& S = *reinterpret_cast<StepSolveSmem<NE>*>(smraw);
@@ -766,7 +766,7 @@ __device__ void gram_smem(const double* M, int rows, int n, double* scratch, dou
 }
 
 template <int NE>
-__global__ void __launch_bounds__(NT) k_finish(const DecProb* probs, int kstart, int src_is_a,
+__global__ void __launch_bounds__(NT, 1) k_finish(const DecProb* probs, int kstart, int src_is_a,
                                                DecParams prm) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ __align__(16) unsigned char smraw[];
