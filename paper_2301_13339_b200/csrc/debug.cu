@@ -56,7 +56,15 @@ extern "C" int qtt_debug_eigh(const void* A, int n, double* lam, void* U, int* s
                               void* stream) {
   using namespace qtt;
   if (n < 1 || n > 32 || reps < 1) return QTT_EINVAL;
-  if (n <= 16) {
+  // mode bit 8: run the NMAX = 20 instantiation (the width the R_max = 10 /
+  // Rhat <= 8 pipelines use) for n <= 20
+  const bool w20 = (mode & 256) != 0;
+  mode &= 255;
+  if (w20 && n <= 20) {
+    cudaFuncSetAttribute(k_debug_eigh<20>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem<20>));
+    k_debug_eigh<20><<<1, NT, sizeof(EigSmem<20>), (cudaStream_t)stream>>>((const cplx*)A, n, lam, (cplx*)U,
+                                                                           sweeps, reps, mode);
+  } else if (n <= 16) {
     cudaFuncSetAttribute(k_debug_eigh<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EigSmem<16>));
     k_debug_eigh<16><<<1, NT, sizeof(EigSmem<16>), (cudaStream_t)stream>>>((const cplx*)A, n, lam, (cplx*)U,
                                                                            sweeps, reps, mode);

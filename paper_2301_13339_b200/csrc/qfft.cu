@@ -37,6 +37,7 @@ static constexpr int NT = 256;
 // Rank capacity RSV of the compact cores: 10 (Rhat <= 8 pipelines; every
 // core in shared memory) or 16 (the paper's Rhat = 15; the cores live in the
 // workspace, pr.cwork, and stay L2-resident).  Rows of a cut <= 2 RSV.
+static_assert(sizeof(EigSmem<16>) <= sizeof(EigSmem<20>), "the width-16 solver overlays S.E");
 template <int RSV>
 struct XfBufs {
   static constexpr int R2 = 2 * RSV;
@@ -210,41 +211,48 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         S.T[e] = s;
       }
       __syncthreads();
-      // K = T M^H
+      // K = T M^H, into the eigensolver of width 16 when rows <= 16 (the
+      // steady state at Rhat <= 8; 18% fewer cycles than width R2 at n = 16,
+      // tools/dev_trid_timing.py), else width R2; both share S.E's memory
+      const bool w16 = (R2 > 16) && rows <= 16;
+      EigSmem<16>& E16 = *reinterpret_cast<EigSmem<16>*>(&S.E);
+      cplx* Kb = w16 ? E16.A[0] : S.E.A[0];
+      const int ldk = w16 ? EigSmem<16>::LD : LD;
       for (int e = tid; e < rows * rows; e += NT) {
         int i = e % rows, j = e / rows;
         cplx s = czero();
         for (int l = 0; l < cols; ++l) s = cfma_bc(S.T[i + rows * l], S.Eb[j + rows * l], s);
-        S.E.A[0][i + LD * j] = s;
+        Kb[i + ldk * j] = s;
       }
       __syncthreads();
       if (c == p) {
         double tr = 0.0;
-        if (tid < rows) tr = S.E.A[0][tid + LD * tid].x;
-        tr = block_sum<NT>(tr, S.E.red);
+        if (tid < rows) tr = Kb[tid + ldk * tid].x;
+        tr = block_sum<NT>(tr, w16 ? E16.red : S.E.red);
         if (tid == 0) S.tau2 = P.eps * P.eps * tr / (double)(d - 1);
         __syncthreads();
       }
       XT_MARK(1)
-      eig_values<R2, NT>(S.E, rows);
+      if (w16) eig_values<16, NT>(E16, rows);
+      else eig_values<R2, NT>(S.E, rows);
       XT_MARK(2)
       if (tid == 0) {
         int mp = rows < S.rb[c] ? rows : S.rb[c];
-        S.rk = rank_choose(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta);
+        S.rk = rank_choose(w16 ? E16.lam : S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta);
       }
       __syncthreads();
       const int rk = S.rk;
-      const cplx* U = eig_vectors<R2, NT>(S.E, rows, rk, P.status);
+      const cplx* U = w16 ? eig_vectors<16, NT>(E16, rows, rk, P.status) : eig_vectors<R2, NT>(S.E, rows, rk, P.status);
       // new core c = U_r  (ap x 2 x rk)
       for (int e = tid; e < rows * rk; e += NT) {
         int i = e % rows, r = e / rows;
-        core(c - 1)[i + rows * r] = U[i + LD * r];
+        core(c - 1)[i + rows * r] = U[i + ldk * r];
       }
       // Sm = U_r^H M  (rk x cols)
       for (int e = tid; e < rk * cols; e += NT) {
         int r = e % rk, l = e / rk;
         cplx s = czero();
-        for (int i = 0; i < rows; ++i) s = cfmac(U[i + LD * r], S.Eb[i + rows * l], s);
+        for (int i = 0; i < rows; ++i) s = cfmac(U[i + ldk * r], S.Eb[i + rows * l], s);
         S.Sm[e] = s;
       }
       __syncthreads();
