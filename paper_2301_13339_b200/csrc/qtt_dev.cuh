@@ -629,25 +629,28 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, const cplx* Qm,
   }
   __syncthreads();
   if (tid == 0) { long long t = clock64(); S.tph[2] = t - tt0; tt0 = t; }
-  // ---- re-orthogonalise clusters (normalised eigenvalues within 1e-4)
-  if (tid == 0) {
+  // ---- re-orthogonalise clusters (normalised eigenvalues within 1e-4):
+  //      modified Gram-Schmidt by warp 0, lane = component (n <= 32)
+  if (tid < 32) {
+    const int i = tid;
     int c0 = 0;
     while (c0 < nvec) {
       int c1 = c0 + 1;
       while (c1 < nvec && S.lam[n - 1 - (c1 - 1)] - S.lam[n - 1 - c1] <= 1e-4) ++c1;
       for (int a = c0 + 1; a < c1; ++a) {
-        double* za = S.Z + LD * a;
+        double za = (i < n) ? S.Z[LD * a + i] : 0.0;
         for (int b = c0; b < a; ++b) {
-          const double* zb = S.Z + LD * b;
-          double d = 0.0;
-          for (int i = 0; i < n; ++i) d += zb[i] * za[i];
-          for (int i = 0; i < n; ++i) za[i] -= d * zb[i];
+          const double zb = (i < n) ? S.Z[LD * b + i] : 0.0;
+          const double d = warp_sum(zb * za);
+          za -= d * zb;
         }
-        double nz = 0.0;
-        for (int i = 0; i < n; ++i) nz += za[i] * za[i];
-        if (!(nz > 1e-6)) S.bad = 1;
-        const double rn = 1.0 / sqrt(nz);
-        for (int i = 0; i < n; ++i) za[i] *= rn;
+        const double nz = warp_sum(za * za);
+        if (!(nz > 1e-6)) {
+          if (i == 0) S.bad = 1;
+        } else if (i < n) {
+          S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
+        }
+        __syncwarp();
       }
       c0 = c1;
     }
