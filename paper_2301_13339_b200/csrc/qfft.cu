@@ -47,6 +47,7 @@ struct XfBufs {
   cplx T[2 * R2 * R2];
   cplx Sm[RSV * R2];
   EigSmem<R2> E;
+  cplx phtab[32];            // phtab[k] = exp(-i pi / 2^k)
   int r[MAXD + 1];
   int rb[MAXD + 1];
   int rk;
@@ -59,11 +60,13 @@ struct XfSmem : XfBufs<RSV> {
 template <int RSV>
 struct XfSmem<RSV, false> : XfBufs<RSV> {};
 
-// twiddle of position q (1-based) in the stage of axis a, bit t, slice be
-__device__ __forceinline__ cplx phi_of(const XfParams& P, int q, int a, int t, int be) {
+// twiddle of position q (1-based) in the stage of axis a, bit t, slice be:
+// exp(-i pi / 2^k), k = bit(q) - t >= 1, from the per-CTA table S.phtab
+// (filled once per launch; a double sincospi per use sat on the chain)
+template <class SM>
+__device__ __forceinline__ cplx phi_of(const SM& S, const XfParams& P, int q, int a, int t, int be) {
   if (be == 0 || P.axis[q - 1] != a) return cmk(1.0, 0.0);
-  const int k = P.bit[q - 1] - t;   // >= 1
-  return cexpipi(-1.0 / (double)(1 << k));
+  return S.phtab[P.bit[q - 1] - t];
 }
 
 // doubled core of position q (p < q <= d) of the current stage into S.D;
@@ -72,7 +75,7 @@ template <class SM>
 __device__ void build_doubled(SM& S, const cplx* c, const XfParams& P, int q, int a, int t) {
   const int d = P.d;
   const int a0 = S.r[q - 1], b0 = S.r[q];
-  const cplx ph = phi_of(P, q, a, t, 1);
+  const cplx ph = phi_of(S, P, q, a, t, 1);
   if (q < d) {
     const int rows = 2 * a0, cols = 2 * b0;
     for (int e = threadIdx.x; e < rows * 2 * cols; e += NT) {
@@ -96,6 +99,23 @@ __device__ void build_doubled(SM& S, const cplx* c, const XfParams& P, int q, in
   }
 }
 
+// sum_{l0 <= l < l1} of f(l, acc) (a complex FMA into acc) over four
+// independent accumulators: the small products of a cut are latency-bound
+// on their dependent FMA chains
+template <class F>
+__device__ __forceinline__ cplx dot4(int l0, int l1, F f) {
+  cplx s0 = czero(), s1 = czero(), s2 = czero(), s3 = czero();
+  int l = l0;
+  for (; l + 3 < l1; l += 4) {
+    s0 = f(l, s0);
+    s1 = f(l + 1, s1);
+    s2 = f(l + 2, s2);
+    s3 = f(l + 3, s3);
+  }
+  for (; l < l1; ++l) s0 = f(l, s0);
+  return cadd(cadd(s0, s1), cadd(s2, s3));
+}
+
 template <int RSV>
 __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfParams P) {
   const XfProb& pr = probs[blockIdx.x];
@@ -109,8 +129,9 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
   };
   const int tid = threadIdx.x;
   const int d = P.d;
-  // load (conj for the inverse)
+  // load (conj for the inverse); twiddle table
   for (int q = tid; q <= d; q += NT) S.r[q] = pr.in_ranks[q];
+  if (tid < 32) S.phtab[tid] = tid == 0 ? cmk(1.0, 0.0) : cexpipi(-ldexp(1.0, -tid));
   __syncthreads();
   for (int q = 0; q < d; ++q) {
     const int n = S.r[q] * 2 * S.r[q + 1];
@@ -153,22 +174,29 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       build_doubled(S, core(c - 1), P, c, a, t);
       __syncthreads();
       const int rows = 2 * S.r[c - 1], cols = 2 * S.r[c];
-      // T[be] = D[be] G   (rows x cols)
+      // T[be] = D[be] G   (rows x cols); D is block diagonal (doubled core):
+      // row i < a0 has columns [0, b0), row i >= a0 columns [b0, 2 b0)
+      const int a0c = S.r[c - 1], b0c = S.r[c];
+      const cplx* Gc = S.G[gc];
       for (int e = tid; e < 2 * rows * cols; e += NT) {
         int i = e % rows, be = (e / rows) & 1, j = e / (2 * rows);
-        cplx s = czero();
-        for (int l = 0; l < cols; ++l)
-          s = cfma(S.D[i + rows * be + 2 * rows * l], S.G[gc][l + cols * j], s);
-        S.T[i + rows * j + rows * cols * be] = s;
+        const int l0 = i < a0c ? 0 : b0c;
+        const cplx* Dr = S.D + i + rows * be;
+        S.T[i + rows * j + rows * cols * be] =
+            dot4(l0, l0 + b0c, [&](int l, cplx acc) { return cfma(Dr[2 * rows * l], Gc[l + cols * j], acc); });
       }
       __syncthreads();
-      // Gn = sum_be T[be] D[be]^H
+      // Gn = sum_be T[be] D[be]^H (columns of D[j] in the block of row j)
       for (int e = tid; e < rows * rows; e += NT) {
         int i = e % rows, j = e / rows;
-        cplx s = czero();
-        for (int be = 0; be < 2; ++be)
-          for (int l = 0; l < cols; ++l)
-            s = cfma_bc(S.T[i + rows * l + rows * cols * be], S.D[j + rows * be + 2 * rows * l], s);
+        const int l0 = j < a0c ? 0 : b0c;
+        const cplx* T0 = S.T + i;
+        const cplx* T1 = S.T + i + rows * cols;
+        const cplx* D0 = S.D + j;
+        const cplx* D1 = S.D + j + rows;
+        const cplx s = cadd(
+            dot4(l0, l0 + b0c, [&](int l, cplx acc) { return cfma_bc(T0[rows * l], D0[2 * rows * l], acc); }),
+            dot4(l0, l0 + b0c, [&](int l, cplx acc) { return cfma_bc(T1[rows * l], D1[2 * rows * l], acc); }));
         S.G[gc ^ 1][e] = s;
         pr.gr[(size_t)(c - 1) * GRS + e] = s;
       }
@@ -206,9 +234,9 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       // T = M G  (rows x cols), M = Eb (ld rows)
       for (int e = tid; e < rows * cols; e += NT) {
         int i = e % rows, j = e / rows;
-        cplx s = czero();
-        for (int l = 0; l < cols; ++l) s = cfma(S.Eb[i + rows * l], S.G[0][l + cols * j], s);
-        S.T[e] = s;
+        const cplx* Er = S.Eb + i;
+        const cplx* Gj = S.G[0] + cols * j;
+        S.T[e] = dot4(0, cols, [&](int l, cplx acc) { return cfma(Er[rows * l], Gj[l], acc); });
       }
       __syncthreads();
       // K = T M^H, into the eigensolver of width 16 when rows <= 16 (the
@@ -220,9 +248,9 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       const int ldk = w16 ? EigSmem<16>::LD : LD;
       for (int e = tid; e < rows * rows; e += NT) {
         int i = e % rows, j = e / rows;
-        cplx s = czero();
-        for (int l = 0; l < cols; ++l) s = cfma_bc(S.T[i + rows * l], S.Eb[j + rows * l], s);
-        Kb[i + ldk * j] = s;
+        const cplx* Ti = S.T + i;
+        const cplx* Ej = S.Eb + j;
+        Kb[i + ldk * j] = dot4(0, cols, [&](int l, cplx acc) { return cfma_bc(Ti[rows * l], Ej[rows * l], acc); });
       }
       __syncthreads();
       if (c == p) {
@@ -251,9 +279,9 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       // Sm = U_r^H M  (rk x cols)
       for (int e = tid; e < rk * cols; e += NT) {
         int r = e % rk, l = e / rk;
-        cplx s = czero();
-        for (int i = 0; i < rows; ++i) s = cfmac(U[i + ldk * r], S.Eb[i + rows * l], s);
-        S.Sm[e] = s;
+        const cplx* Ur = U + ldk * r;
+        const cplx* El = S.Eb + rows * l;
+        S.Sm[e] = dot4(0, rows, [&](int i, cplx acc) { return cfmac(Ur[i], El[i], acc); });
       }
       __syncthreads();
       // next E = Sm * doubled(core c+1)
@@ -271,7 +299,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
             } else {
               for (int i = 0; i < a1; ++i)
                 s = cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be + 2 * a1 * (j - b1)], s);
-              if (be) s = cmul(phi_of(P, q, a, t, 1), s);
+              if (be) s = cmul(phi_of(S, P, q, a, t, 1), s);
             }
             S.Eb[e] = s;
           }
@@ -283,7 +311,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
               s0 = cfma(S.Sm[r + rk * i], cn[i + a1 * be], s0);
               s1 = cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be], s1);
             }
-            if (be) s1 = cmul(phi_of(P, q, a, t, 1), s1);
+            if (be) s1 = cmul(phi_of(S, P, q, a, t, 1), s1);
             S.Eb[e] = cadd(s0, s1);
           }
         }
