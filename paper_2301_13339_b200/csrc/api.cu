@@ -396,7 +396,27 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.tau2 = cv.take<double>(1);
   }
   HrProb* hp = big ? nullptr : cv.take<HrProb>(nf);
-  HrBigProb* hbp = big ? cv.take<HrBigProb>(nf) : nullptr;
+  HrBigProb* hbp = cv.take<HrBigProb>(nf);
+  // multi-CTA chain for few long tensors (C2-C4: 1.04 -> 0.87 ms at d = 18);
+  // a batch already fills the GPU with one CTA per tensor, and short chains
+  // are launch-bound (C1 d = 12, C5 64 tensors: the in-CTA chain is faster)
+  const bool gr_multi = !big && nf <= 8 && d >= 16;
+  if (gr_multi) {
+    // the one-CTA rounding's right-Gram chain runs as multi-CTA mode products
+    // (launch_hr_gr_chain) into its GR slots
+    for (int i = 0; i < nf; ++i) {
+      HrBigProb& q = hb.emplace_back();
+      q = HrBigProb{};
+      q.f_cores = hr[i].f_cores;
+      q.f_ranks = hr[i].f_ranks;
+      q.g_cores = hr[i].g_cores;
+      q.g_ranks = hr[i].g_ranks;
+      q.gr = hr[i].gr;
+      q.t1 = cv.take<cplx>((size_t)6 * GR_HR);
+      q.t2 = q.t1 + 2 * GR_HR;
+      q.t3 = q.t2 + 2 * GR_HR;
+    }
+  }
   std::vector<XfProb> iv(nf);
   for (int i = 0; i < nf; ++i) {
     XfProb& p = iv[i];
@@ -409,7 +429,7 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
     p.do_center = 0;
   }
   if (cv.base) {
-    HrParams H{d, fft->eps, fft->rmax, fft->cluster_tol, status, fft->rule, fft->delta};
+    HrParams H{d, fft->eps, fft->rmax, fft->cluster_tol, status, fft->rule, fft->delta, gr_multi ? 1 : 0};
     if (big) {
       if ((r = cuda_check(cudaMemcpyAsync(hbp, hb.data(), nf * sizeof(HrBigProb), cudaMemcpyHostToDevice, st),
                           "copy descriptors")))
@@ -419,6 +439,12 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
       if ((r = cuda_check(cudaMemcpyAsync(hp, hr.data(), nf * sizeof(HrProb), cudaMemcpyHostToDevice, st),
                           "copy descriptors")))
         return r;
+      if (gr_multi) {
+        if ((r = cuda_check(cudaMemcpyAsync(hbp, hb.data(), nf * sizeof(HrBigProb), cudaMemcpyHostToDevice, st),
+                            "copy descriptors")))
+          return r;
+        if ((r = cuda_check(launch_hr_gr_chain(hbp, nf, d, st), "right-Gram chain launch"))) return r;
+      }
       if ((r = cuda_check(launch_hadamard_round(hp, nf, H, st), "hadamard/round launch"))) return r;
     }
     prof_mark(3, st);

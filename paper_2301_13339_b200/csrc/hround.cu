@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
   const int d = P.d;
   for (int q = tid; q <= d; q += NT) { S.rf[q] = pr.f_ranks[q]; S.rg[q] = pr.g_ranks[q]; }
   __syncthreads();
-  // ---------------- right Gram chain
+  // ---------------- right Gram chain (unless launch_hr_gr_chain computed it
+  //                  with the mode products spread over the GPU)
+  if (!P.gr_ready) {
   {
     // GR_{d-1} = sum_al z z^H, z[(a,a')] = F_d[a,al] G_d[a',al]
     const int af = S.rf[d - 1], ag = S.rg[d - 1], rz = af * ag;
@@ -126,6 +128,7 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
       if (e < rzo * rzo) pr.gr[(size_t)(c - 1) * GR_HR + e] = acc[k];
     }
     __syncthreads();
+  }
   }
   // ---------------- LQ rank bounds
   if (tid == 0) {

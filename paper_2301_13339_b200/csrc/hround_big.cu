@@ -28,7 +28,9 @@ __device__ __forceinline__ const cplx* fcore(const HrBigProb& p, int q) { return
 __device__ __forceinline__ const cplx* gcore(const HrBigProb& p, int q) { return p.g_cores + (size_t)(q - 1) * SLOT; }
 
 // ------------------------------------------------------ right Gram chain
-__global__ void k_hrb_gr_last(const HrBigProb* probs, int d) {
+// gs: complex entries per GR slot and per mode-product slice (RZB^2 for the
+// multi-CTA rounding, GR_HR when the chain feeds the one-CTA sweep)
+__global__ void k_hrb_gr_last(const HrBigProb* probs, int d, int gs) {
   const HrBigProb& p = probs[blockIdx.y];
   const int af = p.f_ranks[d - 1], ag = p.g_ranks[d - 1], rz = af * ag;
   const int e = blockIdx.x * NT + threadIdx.x;
@@ -43,11 +45,11 @@ __global__ void k_hrb_gr_last(const HrBigProb* probs, int d) {
     const cplx zj = cmul(F[ja + af * al], G[jb + ag * al]);
     s = cfma_bc(zi, zj, s);
   }
-  p.gr[(size_t)(d - 1) * RZB * RZB + e] = s;
+  p.gr[(size_t)(d - 1) * gs + e] = s;
 }
 
 // stage 0..3 = A1, A2, B1, B2 of core c (1-based), grid (RZB*RZB/NT, 2 slices, nprob)
-__global__ void k_hrb_gr_step(const HrBigProb* probs, int c, int stage) {
+__global__ void k_hrb_gr_step(const HrBigProb* probs, int c, int stage, int gs) {
   const HrBigProb& p = probs[blockIdx.z];
   const int fa = p.f_ranks[c - 1], fb = p.f_ranks[c], ga = p.g_ranks[c - 1], gb = p.g_ranks[c];
   const int rzx = fb * gb, rzo = fa * ga, ra = fb * ga;
@@ -55,14 +57,14 @@ __global__ void k_hrb_gr_step(const HrBigProb* probs, int c, int stage) {
   const int e = blockIdx.x * NT + threadIdx.x;
   const cplx* F = fcore(p, c);
   const cplx* G = gcore(p, c);
-  cplx* T1 = p.t1 + (size_t)al * RZB * RZB;
-  cplx* T2 = p.t2 + (size_t)al * RZB * RZB;
-  cplx* T3 = p.t3 + (size_t)al * RZB * RZB;
+  cplx* T1 = p.t1 + (size_t)al * gs;
+  cplx* T2 = p.t2 + (size_t)al * gs;
+  cplx* T3 = p.t3 + (size_t)al * gs;
   if (stage == 0) {
     if (e >= ra * rzx) return;
     const int i = e % ra, j = e / ra;
     const int b = i / ga, ap = i % ga;
-    const cplx* X = p.gr + (size_t)c * RZB * RZB + (size_t)(b * gb) + (size_t)rzx * j;
+    const cplx* X = p.gr + (size_t)c * gs + (size_t)(b * gb) + (size_t)rzx * j;
     cplx s = czero();
     for (int bp = 0; bp < gb; ++bp) s = cfma(G[ap + ga * al + 2 * ga * bp], X[bp], s);
     T1[i + ra * j] = s;
@@ -87,11 +89,11 @@ __global__ void k_hrb_gr_step(const HrBigProb* probs, int c, int stage) {
     const int ee = j / ga, ep = j % ga;
     cplx s = czero();
     for (int a2 = 0; a2 < 2; ++a2) {
-      const cplx* T3a = p.t3 + (size_t)a2 * RZB * RZB;
+      const cplx* T3a = p.t3 + (size_t)a2 * gs;
       for (int cc = 0; cc < fb; ++cc)
         s = cfma_bc(T3a[i + rzo * (cc * ga + ep)], F[ee + fa * a2 + 2 * fa * cc], s);
     }
-    p.gr[(size_t)(c - 1) * RZB * RZB + i + rzo * j] = s;
+    p.gr[(size_t)(c - 1) * gs + i + rzo * j] = s;
   }
 }
 
@@ -244,18 +246,32 @@ size_t hr_big_scratch(int d) {
   return (size_t)d * RZB * RZB + 6 * (size_t)RZB * RZB + 4 * (size_t)RWB * RZB;
 }
 
-cudaError_t launch_hadamard_round_big(const HrBigProb* probs_dev, int nprob, const HrParams& prm, cudaStream_t st) {
-  const int d = prm.d;
-  const int g2 = (RZB * RZB + NT - 1) / NT;
+static int launch_hr_gr_chain_impl(const HrBigProb* probs_dev, int nprob, int d, int gs, cudaStream_t st) {
+  const int g2 = (gs + NT - 1) / NT;
   int n = 0;
-  k_hrb_gr_last<<<dim3(g2, nprob), NT, 0, st>>>(probs_dev, d);
+  k_hrb_gr_last<<<dim3(g2, nprob), NT, 0, st>>>(probs_dev, d, gs);
   ++n;
   for (int c = d - 1; c >= 2; --c) {
     for (int stage = 0; stage < 4; ++stage) {
-      k_hrb_gr_step<<<dim3(g2, 2, nprob), NT, 0, st>>>(probs_dev, c, stage);
+      k_hrb_gr_step<<<dim3(g2, 2, nprob), NT, 0, st>>>(probs_dev, c, stage, gs);
       ++n;
     }
   }
+  return n;
+}
+
+// The right-Gram chain alone for the one-CTA rounding (Kronecker ranks <= 64):
+// GR slots of GR_HR entries (the layout k_hadamard_round reads), t1..t3 of
+// 2 x GR_HR each.  ~4 (d - 2) launches, every mode product spread over the GPU.
+cudaError_t launch_hr_gr_chain(const HrBigProb* probs_dev, int nprob, int d, cudaStream_t st) {
+  const int n = launch_hr_gr_chain_impl(probs_dev, nprob, d, GR_HR, st);
+  count_launches(n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hadamard_round_big(const HrBigProb* probs_dev, int nprob, const HrParams& prm, cudaStream_t st) {
+  const int d = prm.d;
+  int n = launch_hr_gr_chain_impl(probs_dev, nprob, d, RZB * RZB, st);
   k_hrb_init<<<nprob, NT, 0, st>>>(probs_dev, d);
   ++n;
   const int gt = (RWB * RZB + NT - 1) / NT, gh = (RB * RB * 2 * RB + NT - 1) / NT;

@@ -131,6 +131,7 @@ struct HrParams {
   int* status;
   int rule;
   double delta;
+  int gr_ready;      // 1: pr.gr already holds the right-Gram chain (launch_hr_gr_chain)
 };
 static constexpr int GR_HR = 64 * 64;
 cudaError_t setup_hr_kernels();
@@ -158,6 +159,9 @@ struct HrBigProb {
 cudaError_t setup_hr_big_kernels();
 size_t hr_big_scratch(int d);   // complex entries of gr + t1..t3 + e, tb, sm, hb
 cudaError_t launch_hadamard_round_big(const HrBigProb* probs_dev, int nprob, const HrParams& prm, cudaStream_t st);
+// right-Gram chain of Z = F (.) G into GR_HR slots (p.gr) for k_hadamard_round
+// (HrParams::gr_ready = 1); uses f/g cores, ranks, gr, t1, t2, t3 of HrBigProb
+cudaError_t launch_hr_gr_chain(const HrBigProb* probs_dev, int nprob, int d, cudaStream_t st);
 
 // -------------------------------------------------------------- expansion
 struct ExProb {
