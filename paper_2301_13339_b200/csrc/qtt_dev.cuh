@@ -47,6 +47,23 @@ __device__ __forceinline__ cplx cexpipi(double x) {
   return make_double2(c, s);
 }
 
+// sum_{l0 <= l < l1} of f(l, acc) (a complex FMA into acc) over four
+// independent accumulators: the small products of a cut are latency-bound
+// on their dependent FMA chains
+template <class F>
+__device__ __forceinline__ cplx dot4(int l0, int l1, F f) {
+  cplx s0 = czero(), s1 = czero(), s2 = czero(), s3 = czero();
+  int l = l0;
+  for (; l + 3 < l1; l += 4) {
+    s0 = f(l, s0);
+    s1 = f(l + 1, s1);
+    s2 = f(l + 2, s2);
+    s3 = f(l + 3, s3);
+  }
+  for (; l < l1; ++l) s0 = f(l, s0);
+  return cadd(cadd(s0, s1), cadd(s2, s3));
+}
+
 // ------------------------------------------------------------ layout maps
 // QTT index q (LSB first) -> element offset in the caller's array.
 //   1D / concat: offset = q (row-major image, x fastest, x bits first).
