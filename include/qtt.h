@@ -17,7 +17,11 @@
  *   - Pointers are DEVICE pointers unless the name ends in _host.
  *   - Every call is stream-ordered on `stream` (a cudaStream_t passed as
  *     void*; NULL = legacy default stream).  Calls do not synchronise the
- *     host unless documented ("syncs").
+ *     host unless documented ("syncs").  qtt_conv_full on one image forks
+ *     the decomposition of g onto a library-owned non-blocking stream of the
+ *     current device and joins it back with events before Step 3, so all
+ *     of its work stays ordered after earlier and before later work on
+ *     `stream` (also under CUDA graph capture: fork/join by events).
  *   - No call allocates device memory: all scratch and all device storage of
  *     TT handles is carved from the caller's workspace `ws` (>= the size
  *     returned by qtt_workspace_bytes, 256-byte aligned).  The workspace must
