@@ -21,7 +21,8 @@
  *     the decomposition of g onto a library-owned non-blocking stream of the
  *     current device and joins it back with events before Step 3, so all
  *     of its work stays ordered after earlier and before later work on
- *     `stream` (also under CUDA graph capture: fork/join by events).
+ *     `stream`.  Calls copy small descriptor arrays from host memory
+ *     (cudaMemcpyAsync); they are not meant for CUDA graph capture.
  *   - No call allocates device memory: all scratch and all device storage of
  *     TT handles is carved from the caller's workspace `ws` (>= the size
  *     returned by qtt_workspace_bytes, 256-byte aligned).  The workspace must
