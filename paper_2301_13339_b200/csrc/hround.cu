@@ -12,6 +12,18 @@
 
 namespace qtt {
 
+// optional sweep phase timing (-DQTT_HR_TIMING): cycles of CTA 0 per phase,
+// written to the tail of the GR scratch (diagnostic builds only)
+#ifdef QTT_HR_TIMING
+#define HT_DECL long long ht_t0 = clock64(), ht_acc[6] = {0, 0, 0, 0, 0, 0};
+#define HT_MARK(k) { long long _t = clock64(); ht_acc[k] += _t - ht_t0; ht_t0 = _t; }
+#define HT_DUMP(ptr) if (threadIdx.x == 0 && blockIdx.x == 0) printf("hround sweep cycles: loadGR %lld T+K %lld eigval %lld rank/vec/core/Sm %lld push %lld loop %lld\n", ht_acc[0], ht_acc[1], ht_acc[2], ht_acc[3], ht_acc[4], ht_acc[5]);
+#else
+#define HT_DECL
+#define HT_MARK(k)
+#define HT_DUMP(ptr)
+#endif
+
 static constexpr int NT = 512;   // one CTA per SM (190 KB smem): more warps to hide the product latencies
 static constexpr int RH = RH_MAX;       // 8
 static constexpr int RZ = RH * RH;      // 64
@@ -153,10 +165,13 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     __syncthreads();
   }
   int ap = 1;
+  HT_DECL
   for (int c = 1; c <= d - 1; ++c) {
     const int rows = 2 * ap, rz = S.rf[c] * S.rg[c];
+    HT_MARK(5)
     for (int e = tid; e < rz * rz; e += NT) S.Y[e] = pr.gr[(size_t)c * GR_HR + e];
     __syncthreads();
+    HT_MARK(0)
     for (int e = tid; e < rows * rz; e += NT) {
       int i = e % rows, j = e / rows;
       cplx s = czero();
@@ -178,7 +193,9 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
       if (tid == 0) S.tau2 = P.eps * P.eps * tr / (double)(d - 1);
       __syncthreads();
     }
+    HT_MARK(1)
     eig_values<2 * RH, NT>(S.E, rows);
+    HT_MARK(2)
     if (tid == 0) {
       int mp = rows < S.rb[c] ? rows : S.rb[c];
       S.rk = rank_choose(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta);
@@ -197,6 +214,7 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
       for (int i = 0; i < rows; ++i) s = cfmac(U[i + LD * r], S.Eb[i + rows * l], s);
       S.Sm[e] = s;
     }
+    HT_MARK(3)
     // next core's F and G
     const int q = c + 1;
     const int fa = S.rf[q - 1], fb = S.rf[q], ga = S.rg[q - 1], gb = S.rg[q];
@@ -226,7 +244,9 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     }
     __syncthreads();
     ap = rk;
+    HT_MARK(4)
   }
+  HT_DUMP(pr.gr + (size_t)MAXD * GR_HR - 8)
   cplx* oc = pr.out_cores + (size_t)(d - 1) * SLOT;
   for (int e = tid; e < 2 * ap; e += NT) oc[e] = S.Eb[e];
   for (int q = tid; q <= d; q += NT) pr.out_ranks[q] = (q == 0 || q == d) ? 1 : S.r[q];
