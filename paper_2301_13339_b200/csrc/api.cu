@@ -1028,17 +1028,20 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
     if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), h.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
                         "copy descriptors")))
       return r;
-    cudaStream_t side = (nf + ng == 2) ? side_stream() : nullptr;
+    const int ntot = nf + ng;
+    cudaStream_t side = ntot >= 2 ? side_stream() : nullptr;
     if (side) {
-      // f on the caller's stream, g on the side stream (fork / join events):
+      // the first half of the tensors (f, or the first batch entries) on the
+      // caller's stream, the rest on the side stream (fork / join events):
       // the one-CTA solves of one chain run under the HBM passes of the other
+      const int na = (ntot + 1) / 2;
       cudaEvent_t fork = nullptr, join = nullptr;
       if ((r = cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event"))) return r;
       if ((r = cuda_check(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "event"))) return r;
       cudaEventRecord(fork, st);
       cudaStreamWaitEvent(side, fork, 0);
-      if ((r = cuda_check(launch_ttsvd(dp + 1, 1, d_, prm, side, 4), "TT-SVD launch"))) return r;
-      if ((r = cuda_check(launch_ttsvd(dp, 1, d_, prm, st, 4), "TT-SVD launch"))) return r;
+      if ((r = cuda_check(launch_ttsvd(dp + na, ntot - na, d_, prm, side, 4), "TT-SVD launch"))) return r;
+      if ((r = cuda_check(launch_ttsvd(dp, na, d_, prm, st, 4), "TT-SVD launch"))) return r;
       cudaEventRecord(join, side);
       if ((r = cuda_check(cudaStreamWaitEvent(st, join, 0), "join"))) return r;
       cudaEventDestroy(fork);

@@ -942,7 +942,10 @@ static inline int per_problem(uint64_t nchunks, int nprob) {
   const int grid_target = 4 * sm_count();
   uint64_t want = (uint64_t)((grid_target + nprob - 1) / nprob);
   if (want > (uint64_t)NBLK_MAX) want = NBLK_MAX;
-  if (t_grid_cap > 0 && want > (uint64_t)t_grid_cap) want = t_grid_cap;
+  if (t_grid_cap > 0) {   // the whole launch stays within the resident slots minus the reserve
+    const uint64_t cap = (uint64_t)(t_grid_cap / nprob > 0 ? t_grid_cap / nprob : 1);
+    if (want > cap) want = cap;
+  }
   if (want > nchunks) want = nchunks;
   return want < 1 ? 1 : (int)want;
 }
