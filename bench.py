@@ -467,6 +467,13 @@ def run_ours(a):
         roof = {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP64_PEAK_TFLOPS if ach else None, "traffic": traffic,
                 "kernel": dom, "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
+        # context: the chain kernels run one CTA (one SM) per tensor, a
+        # latency-bound sequence of d(d-1)/2 dependent truncations; the same
+        # FLOPs against the FP64 peak of the SMs they occupy
+        ctas = {"qfft": nf + ng, "qifft": nf, "hadamard_round": nf}.get(dom)
+        if ctas and ach:
+            roof["sms_used"] = ctas
+            roof["frac_of_used_sms"] = ach / (FP64_PEAK_TFLOPS * ctas / 148.0)
     passes = {}
     for k in ("ttsvd", "expand"):
         if k in stages and stages[k] > 0:
