@@ -1079,7 +1079,13 @@ __device__ const cplx* eig_vectors(EigSmem<NMAX>& E, int n, int k, int* status) 
     const int i = e % n, j = e / n;
     E.A[0][i + LD * j] = E.A[1][i + LD * j];
   }
-  if (threadIdx.x == 0) { E.fallbacks++; raise_status(status, ST_FALLBACK); }
+  if (threadIdx.x == 0) {
+    E.fallbacks++;
+    raise_status(status, ST_FALLBACK);
+#ifdef QTT_FALLBACK_TRACE
+    printf("fallback n=%d k=%d NMAX=%d lam0=%g lam_k=%g\n", n, k, NMAX, E.lam[0], E.lam[k > 0 ? k - 1 : 0]);
+#endif
+  }
   __syncthreads();
   return jacobi_eig<NMAX, NT>(E, n, status);
 }
