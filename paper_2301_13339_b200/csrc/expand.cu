@@ -166,6 +166,16 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
   if (tid < R) S.stack[d][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
   for (int k = tid; k <= d; k += NT) S.rk[k] = pr.ranks[k];
   if constexpr (R <= 8) {
+    // cores 9..15 (<= 7 x 2 R^2 complex) staged in a tree buffer first: the
+    // products below then read shared memory instead of chains of L2 loads
+    cplx* mc = S.tree[0];
+    static_assert(7 * 2 * R * R <= NCOL * R, "mid cores fit a tree buffer");
+    for (int e = tid; e < 7 * 2 * R * R; e += NT) {
+      const int m = e / (2 * R * R), o = e % (2 * R * R);
+      mc[e] = pr.cores[(size_t)(ME + m) * SLOT + o];   // core 9 + m
+    }
+    __syncthreads();
+    auto mcore = [&](int k) -> const cplx* { return mc + (size_t)(k - ME - 1) * 2 * R * R; };
     // Q_a[ha] (r_11 x r_13) = C_12[b12] C_13[b13]; Q_b[hh] (r_13 x r_15) = C_14[b14] C_15[b15]
     for (int e = tid; e < 2 * 4 * R * R; e += NT) {
       const int which = e / (4 * R * R), o = e % (4 * R * R);
@@ -174,8 +184,8 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       const int ra = pr.ranks[k0 - 1], rm = pr.ranks[k0], rb = pr.ranks[k0 + 1];
       cplx acc = czero();
       if (i < ra && j < rb) {
-        const cplx* c0 = pr.cores + (size_t)(k0 - 1) * SLOT;
-        const cplx* c1 = pr.cores + (size_t)k0 * SLOT;
+        const cplx* c0 = mcore(k0);
+        const cplx* c1 = mcore(k0 + 1);
         const int b0 = h & 1, b1 = h >> 1;
         for (int a = 0; a < rm; ++a) acc = cfma(c0[i + ra * b0 + 2 * ra * a], c1[a + rm * b1 + 2 * rm * j], acc);
       }
@@ -183,9 +193,9 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
     }
     // P_low[lb] (r_8 x r_11) = C_9[b9] C_10[b10] C_11[b11], lb = b9 + 2 b10 + 4 b11
     const int q8 = pr.ranks[8], q9 = pr.ranks[9], q10 = pr.ranks[10], q11 = pr.ranks[11];
-    const cplx* c9 = pr.cores + (size_t)8 * SLOT;
-    const cplx* c10 = pr.cores + (size_t)9 * SLOT;
-    const cplx* c11 = pr.cores + (size_t)10 * SLOT;
+    const cplx* c9 = mcore(9);
+    const cplx* c10 = mcore(10);
+    const cplx* c11 = mcore(11);
     for (int e = tid; e < 8 * q8 * q11; e += NT) {
       const int i = e % q8, j = (e / q8) % q11, lb = e / (q8 * q11);
       const int b0 = lb & 1, b1 = (lb >> 1) & 1, b2 = lb >> 2;
