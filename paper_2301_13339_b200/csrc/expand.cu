@@ -110,7 +110,8 @@ static constexpr int RSLD = NCOL + 4;        // ld of Rs rows (columns + pad)
 template <int R>
 struct ExSmem {
   double Rs[2 * R * RSLD];    // [Re R; Im R] (KL x 128), row-major, ld RSLD
-  cplx stack[MAXD + 1][R];    // stack[k-1] = C_k ... C_d (vector of size r_{k-1})
+  cplx stack[MAXD + 2 - TOP0][R];   // stack[k - TOP0] = C_{k+1} ... C_d (size r_k), k >= TOP0 - 1
+  cplx top0c[R <= 8 ? 2 * R * R : 1];  // core TOP0 (its bit flips every super-chunk), R <= 8
   cplx tree[2][NCOL * R];     // mid tree (R > 8); the 2 x 2048-double output stage
   // R <= 8: the 7 mid cores as three products computed once per CTA,
   // P_low[b9 b10 b11] = C_9 C_10 C_11, Q_a[b12 b13] = C_12 C_13 and
@@ -163,7 +164,11 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       int row = 32 * w + 8 * mb + (lane >> 2), col = 4 * ks + (lane & 3);
       afr[mb][ks] = (col < kl) ? pr.lsplit[row + 256 * col] : 0.0;
     }
-  if (tid < R) S.stack[d][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
+  if (tid < R) S.stack[d - TOP0 + 1][tid] = cmk(tid == 0 ? 1.0 : 0.0, 0.0);   // empty product
+  if constexpr (R <= 8) {
+    if (d >= TOP0)
+      for (int e = tid; e < 2 * R * R; e += NT) S.top0c[e] = pr.cores[(size_t)(TOP0 - 1) * SLOT + e];
+  }
   for (int k = tid; k <= d; k += NT) S.rk[k] = pr.ranks[k];
   if constexpr (R <= 8) {
     // cores 9..15 (<= 7 x 2 R^2 complex) staged in a tree buffer first: the
@@ -230,11 +235,11 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       for (int k = hi; k >= TOP0; --k) {
         const int r0 = S.rk[k - 1], r1 = S.rk[k];
         const int be = (int)((c >> (k - TOP0)) & 1);
-        const cplx* core = pr.cores + (size_t)(k - 1) * SLOT;
+        const cplx* core = (R <= 8 && k == TOP0) ? S.top0c : pr.cores + (size_t)(k - 1) * SLOT;
         if (lane < r0) {
           cplx s = czero();
-          for (int j = 0; j < r1; ++j) s = cfma(core[lane + r0 * be + 2 * r0 * j], S.stack[k][j], s);
-          S.stack[k - 1][lane] = s;
+          for (int j = 0; j < r1; ++j) s = cfma(core[lane + r0 * be + 2 * r0 * j], S.stack[k - TOP0 + 1][j], s);
+          S.stack[k - TOP0][lane] = s;
         }
         __syncwarp();
       }
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       //      hb = b12 + 2 b13 + 4 b14 + 8 b15); then all threads:
       //      R[:, col] = P_low[col & 7] u[col >> 3]
       if (w == 0) {
-        const cplx* sv = S.stack[TOP0 - 1];
+        const cplx* sv = S.stack[0];
         const int r11 = S.rk[ME + 3], r13 = S.rk[ME + 5], r15 = S.rk[ME + 7];
         if (lane < 4 * r13) {
           const int i = lane % r13, hh = lane / r13;
@@ -295,7 +300,7 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
     } else {
     __syncthreads();
     // ---- mid tree over cores ME+MB .. ME+1 -> 64 vectors of size r_8
-    const cplx* vin = S.stack[TOP0 - 1];
+    const cplx* vin = S.stack[0];
     int nv = 1, cur = 0;
 #pragma unroll 1
     for (int k = ME + MB; k >= ME + 1; --k) {
