@@ -52,7 +52,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS),
+                    help="headline workload (default c3: the largest config BASELINE.json assigns to one GPU)")
+    ap.add_argument("--extra", default=None,
+                    help="comma-separated configs timed after the headline and attached as extra_configs "
+                         "(default at N=1 with the default headline: c4,c5; 'none' to skip)")
     ap.add_argument("--eps", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -74,6 +78,18 @@ def workload(cfg, eps):
             f"(d={p['d']}, {p['layout']} bits, batch {p['batch']}), eps={e:g}, caps "
             f"(R_max, Rhat_max)=({p['rmax']},{p['rhat']}), periodic conv shift n/2")
     return p, e, desc
+
+
+def config_dict(cfg, desc, world, mode, batch, el_step):
+    """The line's `config`, identical in both arms (same cfg, eps, N)."""
+    p = synth.problem(cfg)
+    par = {"independent": f"independent problems x{world}",
+           "batch": f"batch of {p['batch']} split {world} ways ({batch} images/GPU), no communication",
+           "sharded": f"one problem column-sharded {world} ways (NCCL Gram allreduce + W all-gather)"}[mode]
+    return {"workload": desc, "global_batch": (world * batch if mode != "sharded" else 1),
+            "elements_per_step": el_step * world,
+            "parallelism": par if world > 1 else "single GPU",
+            "l2": "flushed between timed steps (256 MiB write)"}
 
 
 def mode_of(cfg, world):
@@ -250,22 +266,31 @@ def fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, steps, dev, 
 
 
 # ------------------------------------------------------------------- ours
-def run_ours(a):
+def pass_bytes(cfg, rep, nf, ng, n_loc):
+    """Algorithmic bytes of the full-array passes of one qtt_conv_full (SURVEY
+    §8(d)), per pass: level-1 Gram reads every input once; the projection
+    from x reads it again and writes W_5 (r_5 x 2^{d-5}); the first W step
+    reads W_5 and writes W_6; the expansion writes y.  Ranks of batch entry 0
+    stand for every entry (C5 images all reach the cap)."""
+    rf, rg = rep["ranks_f"], rep["ranks_g"]
+    d = len(rf) - 1
+    w5 = 8.0 * (nf * rf[5] + ng * rg[5]) * (n_loc >> 5)
+    w6 = 8.0 * (nf * rf[6] + ng * rg[6]) * (n_loc >> 6)
+    return {"pass_level_gram": 8.0 * (nf + ng) * n_loc,
+            "pass_project_x": 8.0 * (nf + ng) * n_loc + w5,
+            "pass_project_w": w5 + w6,
+            "pass_expand": 8.0 * nf * n_loc} if d > 12 else {}
+
+
+def bench_one(a, cfg, eps, steps, warmup, world, rank, local, dev, full=True):
+    """Time `steps` qtt_conv_full steps of config `cfg` on this rank; returns
+    the JSON line (meaningful on rank 0).  full=False: the headline's timing
+    contract only (no comparator / sweeps / oracle leg)."""
     import torch
     import torch.distributed as dist
-    from paper_2301_13339_b200 import build as B
     from paper_2301_13339_b200 import qtt as Q
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local)
-    B.build()
-    cfg = a.config
-    p, eps, desc = workload(cfg, a.eps)
+    p, eps, desc = workload(cfg, eps)
     mode = mode_of(cfg, world)
     d = p["d"]
     n = 1 << d
@@ -318,9 +343,9 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    def timed(fn, steps):
+    def timed(fn, nsteps):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(steps)]
+               for _ in range(nsteps)]
         for e0, e1 in evs:
             flush.zero_()
             e0.record(stream)
@@ -329,26 +354,26 @@ def run_ours(a):
         torch.cuda.synchronize(dev)
         return sum(e0.elapsed_time(e1) for e0, e1 in evs)
 
-    # correctness guard of this run: numeric status + ranks
+    # correctness guard of this run: numeric status + ranks + T2 margins
     rep = Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, dec, fft, p["shift"],
                           p["scale"], ws.data_ptr(), nb, sp, report=True, comm=comm)
-    for _ in range(a.warmup):
+    for _ in range(warmup):
         step()
     barrier()
     l0 = Q.qtt_launch_count()
     with ClockSampler(local) as clk:
         barrier()
-        ms = timed(step, a.steps)
+        ms = timed(step, steps)
         barrier()
     launches = Q.qtt_launch_count() - l0
     # e2e through host buffers (pinned), copies inside the timed region
-    for _ in range(max(1, a.warmup // 2)):
+    for _ in range(max(1, warmup // 2)):
         e2e_step()
     barrier()
-    ms_e2e = timed(e2e_step, a.steps)
+    ms_e2e = timed(e2e_step, steps)
     barrier()
     # stage profile (separate, untimed-by-the-metric pass)
-    Q.qtt_profile_enable(True)
+    Q.qtt_profile_enable(1)
     stages = {}
     npf = 3
     for _ in range(npf):
@@ -356,21 +381,30 @@ def run_ours(a):
         step()
         for k, v in Q.qtt_profile_read().items():
             stages[k] = stages.get(k, 0.0) + v / npf
-    Q.qtt_profile_enable(False)
-    # dense comparator (paper Tables 2/4 last column): the same
-    # periodic convolution of the same noisy inputs by cuFFT (torch.fft) on this
-    # GPU, inputs resident, L2 flushed, same timing; not part of the metric
+    # full-array pass profile: events around k_level_gram, k_project<true>,
+    # the first k_project<false> and k_expand_main (decomposition as one
+    # chain on this stream for this pass only)
+    Q.qtt_profile_enable(2)
+    pstat = {}
+    for _ in range(npf):
+        flush.zero_()
+        step()
+        for k, v in Q.qtt_profile_read().items():
+            if k.startswith("pass_"):
+                pstat[k] = pstat.get(k, 0.0) + v / npf
+    Q.qtt_profile_enable(0)
     fftc = None
-    if mode != "sharded" and not a.no_fft_comparator:
+    if full and mode != "sharded" and not a.no_fft_comparator:
+        # dense comparator (paper Tables 2/4 last column)
         clean0 = synth.signal(cfg, index=rank * batch if mode == "batch" else rank, noisy=False)
-        fftc = fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, a.steps, dev,
+        fftc = fft_comparator(torch, f_d, g_d, y_d, batch, D, p, timed, flush, steps, dev,
                               clean=np.ascontiguousarray(clean0))
 
     # N4 quality sweep: E2 of the QTT result against the
     # convolution of the CLEAN signal at the caps (10, 8) (default, reading Q4),
     # (10, 15) (the paper's) and (16, 16), with each one's time (--caps-sweep)
     caps_sweep = []
-    if a.caps_sweep and mode != "sharded":
+    if full and a.caps_sweep and mode != "sharded":
         n1 = 1 << p["b"]
         clean0 = np.ascontiguousarray(synth.signal(cfg, index=rank * batch if mode == "batch" else rank,
                                                    noisy=False))
@@ -411,28 +445,28 @@ def run_ours(a):
             for _ in range(2):
                 step2()
             barrier()
-            ms2 = timed(step2, max(2, a.steps // 2))
+            ms2 = timed(step2, max(2, steps // 2))
             r2 = Q.qtt_conv_full(f_d.data_ptr(), g_d.data_ptr(), y_d.data_ptr(), shp, d2, f2, p["shift"],
                                  p["scale"], ws.data_ptr(), nb, sp, report=True, comm=comm)
-            eps_sweep.append({"eps": e2, "ms_per_step": ms2 / max(2, a.steps // 2),
-                              "max_rank_f": max(r2["ranks_f"]), "max_rank_out": max(r2["ranks_out"])})
+            eps_sweep.append({"eps": e2, "ms_per_step": ms2 / max(2, steps // 2),
+                              "max_rank_f": max(r2["ranks_f"]), "max_rank_out": max(r2["ranks_out"]),
+                              "min_margin": r2["min_margin"], "min_gap": r2["min_gap"]})
 
     if world > 1:
         t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ms_e2e = float(t[0]), float(t[1])
     el_step = batch * n_loc                    # elements this rank outputs per step
-    total_el = world * el_step * a.steps       # whole job (all ranks)
+    total_el = world * el_step * steps         # whole job (all ranks)
     value = total_el / (ms / 1e3)
     e2e = total_el / (ms_e2e / 1e3)
-
+    hb = (int(f_h.numel() * 8 + g_h.numel() * 8), int(y_h.numel() * 8))
+    del ws, f_d, g_d, y_d, f_h, g_h, y_h, flush
+    torch.cuda.empty_cache()
+    if comm is not None:
+        comm.close()
     if rank != 0:
-        if comm is not None:
-            comm.close()
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
-        return
+        return None
     hbm, src = peaks()
     ng = 1
     nf = batch
@@ -450,10 +484,9 @@ def run_ours(a):
     traffic = None
     try:
         import glob as _glob
-        caps = sorted(_glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json")))
-        for cp in caps:
+        for cp in sorted(_glob.glob(os.path.join(ROOT, "profiles", "*_ncu_*.json"))):
             cj = json.load(open(cp))
-            if cj.get("stage") == dom:
+            if cj.get("stage") == dom and cj.get("config") in (None, cfg):
                 traffic = cj.get("dram_bytes_per_launch")
     except Exception:
         traffic = None
@@ -480,33 +513,34 @@ def run_ours(a):
             gbs = alg[k][1] / (stages[k] / 1e3) / 1e9
             passes[k] = {"ms": round(stages[k], 4), "alg_GBps": round(gbs, 1),
                          "frac_hbm": round(gbs / hbm, 4)}
-    par = {"independent": f"independent problems x{world}",
-           "batch": f"batch of {p['batch']} split {world} ways ({batch} images/GPU), no communication",
-           "sharded": f"one problem column-sharded {world} ways (NCCL Gram allreduce + W all-gather)"}[mode]
+    kern = {"pass_level_gram": "k_level_gram", "pass_project_x": "k_project<true>",
+            "pass_project_w": "k_project<false> (first W step)", "pass_expand": "k_expand_main"}
+    for k, nbytes in pass_bytes(cfg, rep, nf, ng, n_loc).items():
+        if pstat.get(k, 0.0) > 0:
+            gbs = nbytes / (pstat[k] / 1e3) / 1e9
+            passes[k] = {"kernel": kern[k], "ms": round(pstat[k], 4), "alg_bytes": nbytes,
+                         "alg_GBps": round(gbs, 1), "frac_hbm": round(gbs / hbm, 4)}
     line = {
         "metric": "end-to-end full-array elements/s (decompose+QTT conv+expand), fraction of HBM roofline",
-        "value": value, "unit": "elements/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "value": value, "unit": "elements/s", "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": ms / steps, "higher_is_better": True,
         "scaling": "weak" if mode == "independent" else "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded SAR-like scatterers + sinc kernel, BASELINE.json configs)",
-        "config": {"workload": desc, "global_batch": (world * batch if mode != "sharded" else 1),
-                   "elements_per_step": el_step * world,
-                   "parallelism": par if world > 1 else "single GPU",
-                   "l2": "flushed between timed steps (256 MiB write)"},
-        "hbm_fraction_e2e_floor": (40.0 * el_step * world / (ms / 1e3 / a.steps) / 1e9) / (hbm * world),
+        "config": config_dict(cfg, desc, world, mode, batch, el_step),
+        "hbm_fraction_e2e_floor": (40.0 * el_step * world / (ms / 1e3 / steps) / 1e9) / (hbm * world),
         "e2e": {"value": e2e, "unit": "elements/s",
-                "h2d_bytes_per_step": int(f_h.numel() * 8 + g_h.numel() * 8),
-                "d2h_bytes_per_step": int(y_h.numel() * 8)},
+                "h2d_bytes_per_step": hb[0], "d2h_bytes_per_step": hb[1]},
         "gpu_launches": int(launches),
         "roofline": roof,
         "stages_ms": {k: round(v, 4) for k, v in stages.items()},
         "hbm_passes": passes,
         "clocks": clk.summary(),
         "ranks": {"f": rep["ranks_f"], "g": rep["ranks_g"], "out": rep["ranks_out"]},
+        "t2": {"min_margin": rep["min_margin"], "min_gap": rep["min_gap"]},
         "status_bits": rep["status_bits"],
     }
     if fftc is not None:
-        fftc["qtt_over_fft_time"] = (ms / a.steps) / fftc["ms_per_step"]
+        fftc["qtt_over_fft_time"] = (ms / steps) / fftc["ms_per_step"]
         line["fft_comparator"] = fftc
     if eps_sweep:
         line["eps_sweep"] = eps_sweep
@@ -518,18 +552,63 @@ def run_ours(a):
     chain_ms = stages.get("qfft", 0.0) + stages.get("hadamard_round", 0.0) + stages.get("qifft", 0.0)
     line["chain"] = {"sequential_truncations": 2 * cuts + (d - 1), "ms": round(chain_ms, 4),
                      "us_per_truncation": round(1e3 * chain_ms / (2 * cuts + (d - 1)), 2),
-                     "share_of_step": round(chain_ms / (ms / a.steps), 4)}
-    if not a.no_cpu_baseline and world == 1:
-        if d <= 24:
-            line["cpu_baseline"] = oracle_run(cfg, eps, a.cpu_seconds)
-        else:
-            line["cpu_baseline"] = {"value": None, "unit": "elements/s", "kind": "oracle",
-                                    "cores": len(os.sched_getaffinity(0)),
-                                    "sample": "skipped: one oracle pipeline at d = 28 takes minutes "
-                                              "(SURVEY F15), beyond the bounded-sample budget"}
-    print(json.dumps(line), flush=True)
-    if comm is not None:
-        comm.close()
+                     "share_of_step": round(chain_ms / (ms / steps), 4)}
+    return line
+
+
+def stated_oracle(cfg):
+    """The oracle's own time for one pipeline of `cfg`, as measured by
+    tools/make_golden_fullsize.py on the build host (stated, not live)."""
+    try:
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"fullsize_{cfg}.json")))
+        secs = [r["oracle_seconds"] for r in gold["runs"] if r["eps"] == gold["eps"][0]]
+        p = synth.problem(cfg)
+        return {"value": (1 << p["d"]) / (sum(secs) / len(secs)), "unit": "elements/s", "kind": "oracle",
+                "cores": None, "sample": f"stated: mean of {len(secs)} whole oracle pipeline(s) of {cfg} "
+                                         f"({sum(secs) / len(secs):.1f} s each) timed by "
+                                         "tools/make_golden_fullsize.py on the build host, not in this run"}
+    except Exception:
+        return None
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2301_13339_b200 import build as B
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    B.build()
+    line = bench_one(a, a.config, a.eps, a.steps, a.warmup, world, rank, local, dev, full=True)
+    extra = a.extra
+    if extra is None:
+        extra = "c4,c5" if (world == 1 and a.config == "c3" and a.eps is None and a.rhat is None) else "none"
+    extras = {}
+    for cfg in [c for c in extra.split(",") if c and c != "none"]:
+        ex = bench_one(a, cfg, None, max(3, a.steps // 2), max(3, a.warmup), world, rank, local, dev, full=False)
+        if rank == 0:
+            keep = ("value", "unit", "ms_per_step", "steps", "warmup", "config", "e2e", "roofline",
+                    "stages_ms", "hbm_passes", "clocks", "ranks", "t2", "status_bits", "chain",
+                    "hbm_fraction_e2e_floor", "eps_sweep", "gpu_launches", "scaling")
+            extras[cfg] = {k: ex[k] for k in keep if k in ex}
+            so = stated_oracle(cfg)
+            if so is not None:
+                extras[cfg]["cpu_baseline"] = so
+    if rank == 0:
+        if extras:
+            line["extra_configs"] = extras
+        p = synth.problem(a.config)
+        if not a.no_cpu_baseline and world == 1:
+            if p["d"] <= 24:
+                line["cpu_baseline"] = oracle_run(a.config, workload(a.config, a.eps)[1], a.cpu_seconds)
+            else:
+                line["cpu_baseline"] = stated_oracle(a.config)
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -554,9 +633,12 @@ def run_reference(a):
     line = {
         "metric": "end-to-end full-array elements/s (decompose+QTT conv+expand), fraction of HBM roofline",
         "value": v, "unit": "elements/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": el_step / v * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": el_step / v * 1e3, "higher_is_better": True,
+        "scaling": "weak" if mode_of(a.config, a.gpus) == "independent" else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": desc, "global_batch": p["batch"], "elements_per_step": el_step},
+        "config": config_dict(a.config, desc, a.gpus, mode_of(a.config, a.gpus),
+                              p["batch"] // a.gpus if mode_of(a.config, a.gpus) == "batch" else 1,
+                              el_step // a.gpus if mode_of(a.config, a.gpus) != "independent" else el_step),
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -29,7 +29,11 @@
  *     stay alive and untouched while the handles carved from it are used.
  *   - Arrays are float64.  1D: x[i], i = 0..2^b-1.  2D: row-major image
  *     x[iy * 2^bx + ix] (x fastest).  QTT bit order is LSB first;
- *     the 2D mode order is the `layout` field (reading Q8).
+ *     the 2D mode order is the `layout` field (reading Q8).  Input arrays
+ *     (f, g, x) and every batch entry must start on a 16-byte boundary (the
+ *     TT-SVD streams them with 16-byte copies): a misaligned pointer or an
+ *     odd batch stride is QTT_EINVAL.  Outputs (y) may have any 8-byte
+ *     alignment and stride.
  *   - Truncation (reading Q1-Q6): per-cut threshold
  *     tau^2 = eps^2 ||A||_F^2 / (d-1), rank = min(rank_tau, rmax) moved out
  *     of clusters of relative width cluster_tol (Q6').
@@ -113,7 +117,17 @@ typedef struct qtt_tt_s* qtt_tt_t;      /* opaque TT tensor (batch of them)  */
 typedef struct qtt_comm_s* qtt_comm_t;  /* NULL = single GPU                 */
 
 /* Optional report of qtt_conv_full (host struct, filled when non-NULL;
- * filling it syncs the stream).  ranks_*: r_0..r_d of batch entry 0. */
+ * filling it syncs the stream).  ranks_*: r_0..r_d of batch entry 0 of the
+ * signal TT-SVD (f), the kernel TT-SVD (g), their QTT-FFTs (fh, gh), the
+ * rounded Hadamard product (z) and the output (out, after the QTT-iFFT).
+ * min_margin / min_gap: T2 well-posedness evidence over
+ * every eps-rule truncation of the call (all batch entries): the smallest
+ * |T - tau^2| / tau^2 of a deciding tail sum T (T(r_tau) and T(r_tau - 1)
+ * when eps decides, T(R) when the cap does) and the smallest
+ * (lambda_r - lambda_{r+1}) / lambda_1 at a chosen rank r < m; a Gram
+ * eigenvalue carries ~1e3 m eps_mach lambda_1 of absolute noise, so a margin
+ * far above that is a rank decision the SVD oracle takes identically.
+ * Both are +inf when nothing was recorded (eps = 0, drop-off rule). */
 typedef struct {
   int d;
   int ranks_f[64], ranks_g[64], ranks_fh[64], ranks_gh[64], ranks_z[64],
@@ -122,6 +136,8 @@ typedef struct {
   int status_bits;   /* device status word: 1 non-finite input, 2 eigensolver
                         failure (both errors), 16 = a tridiagonal eigensolve
                         fell back to Jacobi (information) */
+  double min_margin;
+  double min_gap;
 } qtt_report;
 
 /* Bytes of workspace needed by qtt_conv_full (and enough for any single

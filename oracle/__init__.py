@@ -32,14 +32,14 @@ Parity status:
                                           Example 1.
 """
 
-from .qtt import (axes_descriptor, to_qtt, from_qtt, rank_rule, rank_rule_dropoff, choose_rank,
+from .qtt import (axes_descriptor, to_qtt, from_qtt, rank_rule, rank_rule_dropoff, choose_rank, margin_log,
                   tt_svd, full, element, storage_count, ranks_of)
 from .qfft import qfft, qifft, center, hadamard, round_full, round_local
 from .conv import conv_pipeline
 from . import rng
 
 __all__ = [
-    "axes_descriptor", "to_qtt", "from_qtt", "rank_rule", "rank_rule_dropoff", "choose_rank",
+    "axes_descriptor", "to_qtt", "from_qtt", "rank_rule", "rank_rule_dropoff", "choose_rank", "margin_log",
     "tt_svd", "full",
     "element", "storage_count", "ranks_of", "qfft", "qifft", "center",
     "hadamard", "round_full", "round_local", "conv_pipeline",

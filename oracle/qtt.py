@@ -116,10 +116,55 @@ def rank_rule(lam, tau2, rmax, cluster_tol):
             while cl(rp):
                 rp += 1
             if rp <= rmax:
+                _log_margin(lam, tail, tau2, r_tau, rmax, rp)
                 return rp
         while r > 1 and cl(r):
             r -= 1
+    _log_margin(lam, tail, tau2, r_tau, rmax, r)
     return r
+
+
+# ---------------------------------------------------------------------------
+# T2 well-posedness diagnostics.  Logging only: nothing here
+# feeds back into a rank or a value.
+# ---------------------------------------------------------------------------
+
+_MARGIN_LOG = None
+
+
+class margin_log:
+    """Context manager: while active, every RANK decision appends
+    (margin, gap) to the list it yields.  margin = distance of the deciding
+    tail sum(s) from tau^2, relative to tau^2 — |T(r_tau) - tau^2| and
+    |T(r_tau - 1) - tau^2| when eps decides (r_tau <= R), |T(R) - tau^2| when
+    the cap does; gap = (lam_r - lam_{r+1}) / lam_1 at the returned r (inf
+    when r = m).  SURVEY §4.2 T2 flags a cut when |T - tau^2| is within the
+    Gram noise (~1e3 m eps_mach lam_1) or the gap within [0.1, 10] delta_c."""
+
+    def __enter__(self):
+        global _MARGIN_LOG
+        self.prev, self.rows = _MARGIN_LOG, []
+        _MARGIN_LOG = self.rows
+        return self.rows
+
+    def __exit__(self, *exc):
+        global _MARGIN_LOG
+        _MARGIN_LOG = self.prev
+        return False
+
+
+def _log_margin(lam, tail, tau2, r_tau, rmax, r):
+    if _MARGIN_LOG is None or not tau2 > 0.0:
+        return
+    m = lam.shape[0]
+    if r_tau <= rmax:
+        mg = abs(tail[r_tau] - tau2)
+        if r_tau > 1:
+            mg = min(mg, abs(tail[r_tau - 1] - tau2))
+    else:
+        mg = abs(tail[rmax] - tau2)
+    gap = (lam[r - 1] - lam[r]) / lam[0] if r < m else float("inf")
+    _MARGIN_LOG.append((mg / tau2, gap))
 
 
 def rank_rule_dropoff(lam, delta, rmax, cluster_tol):

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <atomic>
+#include <cmath>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -21,8 +22,13 @@
 
 using namespace qtt;
 
+namespace {
+extern int g_prof;
+void prof_pass_impl(int pass, int end, cudaStream_t st);
+}
 namespace qtt {
 static std::atomic<long long> g_launches{0};
+void prof_pass(int pass, int end, cudaStream_t st) { prof_pass_impl(pass, end, st); }
 void count_launches(int n) { g_launches += n; }
 int sm_count() {
   static std::atomic<int> cache[64];
@@ -108,20 +114,68 @@ void prof_mark(int i, cudaStream_t st) {
   }
   cudaEventRecord(g_ev[i], st);
 }
+cudaEvent_t g_pev[PASS_N][2] = {};
+int g_pev_ok = 0;
+int g_pev_set[PASS_N] = {};
 
-std::once_flag g_setup_once;
-cudaError_t g_setup_err = cudaSuccess;
+// level 2: events around the first full-array passes of the call (the
+// decomposition then runs as one chain on the caller's stream, so a pass's
+// events bracket that pass alone)
+void prof_pass_impl(int pass, int end, cudaStream_t st) {
+  if (g_prof < 2 || pass < 0 || pass >= PASS_N) return;
+  if (!g_pev_ok) {
+    for (int k = 0; k < PASS_N; ++k) {
+      cudaEventCreate(&g_pev[k][0]);
+      cudaEventCreate(&g_pev[k][1]);
+    }
+    g_pev_ok = 1;
+  }
+  cudaEventRecord(g_pev[pass][end], st);
+  if (end) g_pev_set[pass] = 1;
+}
+
+// cudaFuncSetAttribute (dynamic shared memory above 48 KB) is per device
+// context: done once per device, retried after a failure
+std::mutex g_setup_mu;
+bool g_setup_done[64] = {};
 
 cudaError_t setup_all() {
-  std::call_once(g_setup_once, [] {
-    cudaError_t e;
-    if ((e = setup_ttsvd_kernels()) != cudaSuccess) { g_setup_err = e; return; }
-    if ((e = setup_xf_kernels()) != cudaSuccess) { g_setup_err = e; return; }
-    if ((e = setup_hr_kernels()) != cudaSuccess) { g_setup_err = e; return; }
-    if ((e = setup_hr_big_kernels()) != cudaSuccess) { g_setup_err = e; return; }
-    if ((e = setup_expand_kernels()) != cudaSuccess) { g_setup_err = e; return; }
-  });
-  return g_setup_err;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> lk(g_setup_mu);
+  if (g_setup_done[dev]) return cudaSuccess;
+  if ((e = setup_ttsvd_kernels()) != cudaSuccess) return e;
+  if ((e = setup_xf_kernels()) != cudaSuccess) return e;
+  if ((e = setup_hr_kernels()) != cudaSuccess) return e;
+  if ((e = setup_hr_big_kernels()) != cudaSuccess) return e;
+  if ((e = setup_expand_kernels()) != cudaSuccess) return e;
+  g_setup_done[dev] = true;
+  return cudaSuccess;
+}
+
+// events owned by one call, destroyed on every exit path
+struct EventGuard {
+  cudaEvent_t ev[4] = {};
+  int n = 0;
+  cudaError_t make(cudaEvent_t* out, unsigned flags) {
+    cudaError_t e = cudaEventCreateWithFlags(out, flags);
+    if (e == cudaSuccess) ev[n++] = *out;
+    return e;
+  }
+  ~EventGuard() {
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  }
+};
+
+// The TT-SVD chunk loaders read the inputs with 16-byte cp.async copies
+// (ttsvd.cu load_chunk_async): every array (and every batch entry) must
+// start on a 16-byte boundary.
+qtt_status check_input_align(const double* x, long long stride, int n, const char* which) {
+  if (((uintptr_t)x & 15) != 0) return fail(QTT_EINVAL, "%s must be 16-byte aligned", which);
+  if (n > 1 && (stride & 1)) return fail(QTT_EINVAL, "%s batch stride must be even (16-byte aligned entries)", which);
+  return QTT_OK;
 }
 
 // bump allocator over the caller's workspace (dry run when base == nullptr)
@@ -333,7 +387,8 @@ qtt_status run_expand(const cplx* cores, const int* ranks, int nt, int d, double
 // Step 3 on handles' storage: F (nf tensors), G (ng = 1 or nf) -> Y (nf)
 qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, const int* gr, int ng,
                         const qtt_shape* s, const qtt_trunc* fft, const long long* shift, double scale,
-                        TTAlloc Y, Carver& cv, int* status, cudaStream_t st, int in_rcap) {
+                        TTAlloc Y, Carver& cv, int* status, cudaStream_t st, int in_rcap,
+                        TTAlloc* stages_out = nullptr) {
   const int d = shape_d(s);
   // Rhat <= RH_MAX: one-CTA rounding; above: the multi-CTA variant (Kronecker ranks <= 256)
   const bool big = fft->rmax > RH_MAX;
@@ -342,6 +397,7 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
   TTAlloc Fh = take_tt(cv, nf, d);
   TTAlloc Gh = take_tt(cv, ng, d);
   TTAlloc Z = take_tt(cv, nf, d);
+  if (stages_out) { stages_out[0] = Fh; stages_out[1] = Gh; stages_out[2] = Z; }
   std::vector<XfProb> fw(nf + ng);
   for (int i = 0; i < nf + ng; ++i) {
     const bool isf = i < nf;
@@ -815,9 +871,11 @@ qtt_status qtt_decompose(const double* x, const qtt_shape* shape, const qtt_trun
   if ((r = check_shape(shape))) return r;
   if (!x || !out) return fail(QTT_EINVAL, "x / out is NULL");
   if ((r = check_trunc(dec, comm ? RS_GATHER : RC, "dec", !comm))) return r;
+  const int d = shape_d(shape);
+  if ((r = check_input_align(x, shape->f_stride ? shape->f_stride : (1ll << d), comm ? 1 : shape->batch, "x")))
+    return r;
   cudaError_t ce;
   if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
-  const int d = shape_d(shape);
   if (comm) {
     ShardGeom g;
     if ((r = check_comm(comm, shape, &g))) return r;
@@ -835,7 +893,7 @@ qtt_status qtt_decompose(const double* x, const qtt_shape* shape, const qtt_trun
     if ((r = check_ws(dry, ws, ws_bytes))) return r;
     Carver cv(ws);
     plan(cv, status, tt, D);
-    if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
+    if ((r = cuda_check(cudaMemsetAsync(status, 0, STATUS_BYTES, st), "status reset"))) return r;
     DecParams prm = dec_params(dec, status);
     if ((r = run_sharded_dec(D, comm, prm, st))) return r;
     *out = new_handle(shape, 1, dec->rmax, tt, status, st);
@@ -852,7 +910,7 @@ qtt_status qtt_decompose(const double* x, const qtt_shape* shape, const qtt_trun
   Carver cv(ws);
   status = cv.take<int>(64);
   tt = take_tt(cv, n, d);
-  if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
+  if ((r = cuda_check(cudaMemsetAsync(status, 0, STATUS_BYTES, st), "status reset"))) return r;
   if ((r = run_decompose(x, stride, n, shape, dec, tt, cv, status, st))) return r;
   *out = new_handle(shape, n, dec->rmax, tt, status, st);
   if (!*out) return fail(QTT_ENOMEM, "host allocation failed");
@@ -976,24 +1034,32 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   if (!ws) return fail(QTT_EINVAL, "workspace is NULL");
   if (((uintptr_t)ws & 255) != 0) return fail(QTT_EINVAL, "workspace must be 256-byte aligned");
   if (ws_bytes < need) return fail(QTT_ENOMEM, "workspace too small: need %zu bytes, got %zu", need, ws_bytes);
-  cudaError_t ce;
-  if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
   const int d = shape_d(shape);
   const int nf = shape->batch, ng = shape->g_stride == 0 ? 1 : shape->batch;
   const long long fs = shape->f_stride ? shape->f_stride : (1ll << d);
   const long long gs = shape->g_stride;
   const long long ys = shape->y_stride ? shape->y_stride : (1ll << d);
+  if (!comm) {
+    if ((r = check_input_align(f, fs, nf, "f"))) return r;
+    if ((r = check_input_align(g, gs, ng, "g"))) return r;
+  } else {
+    if ((r = check_input_align(f, 0, 1, "f"))) return r;
+    if ((r = check_input_align(g, 0, 1, "g"))) return r;
+  }
+  cudaError_t ce;
+  if ((ce = setup_all())) return cuda_check(ce, "kernel setup");
   cudaStream_t st = (cudaStream_t)stream;
+  EventGuard evg;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (rep_host) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    if ((r = cuda_check(evg.make(&e0, cudaEventDefault), "event"))) return r;
+    if ((r = cuda_check(evg.make(&e1, cudaEventDefault), "event"))) return r;
     cudaEventRecord(e0, st);
   }
   Carver cv(ws);
   int* status = cv.take<int>(64);
   TTAlloc F = take_tt(cv, nf, d), G = take_tt(cv, ng, d), Y = take_tt(cv, nf, d);
-  if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
+  if ((r = cuda_check(cudaMemsetAsync(status, 0, STATUS_BYTES, st), "status reset"))) return r;
   prof_mark(0, st);
   DecParams prm = dec_params(dec, status);
   if (comm) {
@@ -1029,31 +1095,33 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
                         "copy descriptors")))
       return r;
     const int ntot = nf + ng;
-    cudaStream_t side = ntot >= 2 ? side_stream() : nullptr;
+    cudaStream_t side = (ntot >= 2 && g_prof < 2) ? side_stream() : nullptr;
     if (side) {
       // the first half of the tensors (f, or the first batch entries) on the
       // caller's stream, the rest on the side stream (fork / join events):
       // the one-CTA solves of one chain run under the HBM passes of the other
       const int na = (ntot + 1) / 2;
       cudaEvent_t fork = nullptr, join = nullptr;
-      if ((r = cuda_check(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event"))) return r;
-      if ((r = cuda_check(cudaEventCreateWithFlags(&join, cudaEventDisableTiming), "event"))) return r;
+      if ((r = cuda_check(evg.make(&fork, cudaEventDisableTiming), "event"))) return r;
+      if ((r = cuda_check(evg.make(&join, cudaEventDisableTiming), "event"))) return r;
       cudaEventRecord(fork, st);
       cudaStreamWaitEvent(side, fork, 0);
-      if ((r = cuda_check(launch_ttsvd(dp + na, ntot - na, d_, prm, side, 4), "TT-SVD launch"))) return r;
-      if ((r = cuda_check(launch_ttsvd(dp, na, d_, prm, st, 4), "TT-SVD launch"))) return r;
+      r = cuda_check(launch_ttsvd(dp + na, ntot - na, d_, prm, side, 4), "TT-SVD launch");
+      // the join is recorded even after a failed launch, so `st` never runs
+      // ahead of work already queued on the side stream
+      if (!r) r = cuda_check(launch_ttsvd(dp, na, d_, prm, st, 4), "TT-SVD launch");
       cudaEventRecord(join, side);
-      if ((r = cuda_check(cudaStreamWaitEvent(st, join, 0), "join"))) return r;
-      cudaEventDestroy(fork);
-      cudaEventDestroy(join);
+      qtt_status rj = cuda_check(cudaStreamWaitEvent(st, join, 0), "join");
+      if (r || (r = rj)) return r;
     } else if ((r = cuda_check(launch_ttsvd(dp, nf + ng, d_, prm, st), "TT-SVD launch"))) {
       return r;
     }
   }
   prof_mark(1, st);
   // Step 3
+  TTAlloc mid[3];
   if ((r = run_convolve(F.cores, F.ranks, nf, G.cores, G.ranks, ng, shape, fft, shift, scale, Y, cv, status, st,
-                        dec->rmax)))
+                        dec->rmax, mid)))
     return r;
   // Step 4
   if (comm) {
@@ -1071,14 +1139,28 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
     memset(rep_host, 0, sizeof(*rep_host));
     rep_host->d = d;
     cudaEventElapsedTime(&rep_host->ms_total, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaMemcpy(rep_host->ranks_f, F.ranks, (d + 1) * sizeof(int), cudaMemcpyDeviceToHost);
-    cudaMemcpy(rep_host->ranks_g, G.ranks, (d + 1) * sizeof(int), cudaMemcpyDeviceToHost);
-    cudaMemcpy(rep_host->ranks_out, Y.ranks, (d + 1) * sizeof(int), cudaMemcpyDeviceToHost);
-    int hs = 0;
-    cudaMemcpy(&hs, status, sizeof(int), cudaMemcpyDeviceToHost);
+    const size_t rb = (d + 1) * sizeof(int);
+    cudaMemcpy(rep_host->ranks_f, F.ranks, rb, cudaMemcpyDeviceToHost);
+    cudaMemcpy(rep_host->ranks_g, G.ranks, rb, cudaMemcpyDeviceToHost);
+    cudaMemcpy(rep_host->ranks_fh, mid[0].ranks, rb, cudaMemcpyDeviceToHost);
+    cudaMemcpy(rep_host->ranks_gh, mid[1].ranks, rb, cudaMemcpyDeviceToHost);
+    cudaMemcpy(rep_host->ranks_z, mid[2].ranks, rb, cudaMemcpyDeviceToHost);
+    cudaMemcpy(rep_host->ranks_out, Y.ranks, rb, cudaMemcpyDeviceToHost);
+    int hst[16] = {};
+    cudaMemcpy(hst, status, STATUS_BYTES, cudaMemcpyDeviceToHost);
+    const int hs = hst[0];
     rep_host->status_bits = hs;
+    auto unmin = [](const int* w) {
+      unsigned long long b;
+      memcpy(&b, w, sizeof b);
+      if (!b) return HUGE_VAL;
+      b = ~b;
+      double v;
+      memcpy(&v, &b, sizeof v);
+      return v;
+    };
+    rep_host->min_margin = unmin(hst + 2);
+    rep_host->min_gap = unmin(hst + 4);
     if ((r = cuda_check(cudaGetLastError(), "report"))) return r;
     if (hs & ST_ERRORS) return fail(QTT_ENUMERIC, "numeric status 0x%x (1 = non-finite input, 2 = eigensolver)", hs);
   }
@@ -1109,7 +1191,10 @@ qtt_status qtt_ranks(qtt_tt_t t, int index, int* ranks_host, int cap) {
 
 int qtt_ndims(qtt_tt_t t) { return t ? t->d : 0; }
 
-void qtt_profile_enable(int on) { g_prof = on ? 1 : 0; }
+void qtt_profile_enable(int on) {
+  g_prof = on < 0 ? 0 : (on > 2 ? 2 : on);
+  for (int k = 0; k < PASS_N; ++k) g_pev_set[k] = 0;
+}
 
 int qtt_profile_read(float* ms_host, int n) {
   if (!g_ev_ok || !ms_host || n < PROF_STAGES) return 0;
@@ -1119,7 +1204,13 @@ int qtt_profile_read(float* ms_host, int n) {
     cudaEventElapsedTime(&ms, g_ev[k], g_ev[k + 1]);
     ms_host[k] = ms;
   }
-  return PROF_STAGES;
+  if (n < PROF_STAGES + PASS_N || g_prof < 2) return PROF_STAGES;
+  for (int k = 0; k < PASS_N; ++k) {
+    float ms = -1.f;
+    if (g_pev_set[k]) cudaEventElapsedTime(&ms, g_pev[k][0], g_pev[k][1]);
+    ms_host[PROF_STAGES + k] = ms;
+  }
+  return PROF_STAGES + PASS_N;
 }
 
 long long qtt_launch_count(void) { return qtt::g_launches.load(); }
@@ -1139,7 +1230,7 @@ qtt_status qtt_debug_tt_from_host(const qtt_shape* shape, const void* cores_host
   int* status = cv.take<int>(64);
   TTAlloc tt = take_tt(cv, n, d);
   cudaStream_t st = (cudaStream_t)stream;
-  if ((r = cuda_check(cudaMemsetAsync(status, 0, sizeof(int), st), "status reset"))) return r;
+  if ((r = cuda_check(cudaMemsetAsync(status, 0, STATUS_BYTES, st), "status reset"))) return r;
   if ((r = cuda_check(cudaMemcpyAsync(tt.cores, cores_host, (size_t)n * d * SLOT * sizeof(cplx),
                                       cudaMemcpyHostToDevice, st), "cores upload")))
     return r;

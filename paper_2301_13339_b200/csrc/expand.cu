@@ -455,8 +455,10 @@ cudaError_t launch_expand(const ExProb* probs_dev, int nprob, const ExParams& pr
   if (target < 1) target = 1;
   int per = (int)((nsup + target - 1) / target);
   int nb = (int)((nsup + per - 1) / per);
+  prof_pass(PASS_EXPAND, 0, st);
   if (r8) k_expand_main<8><<<dim3(nb, nprob), NT, sizeof(ExSmem<8>), st>>>(probs_dev, prm, per);
   else k_expand_main<RC><<<dim3(nb, nprob), NT, sizeof(ExSmem<RC>), st>>>(probs_dev, prm, per);
+  prof_pass(PASS_EXPAND, 1, st);
   count_launches(2);
   return cudaGetLastError();
 }

@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     HT_MARK(2)
     if (tid == 0) {
       int mp = rows < S.rb[c] ? rows : S.rb[c];
-      S.rk = rank_choose(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta);
+      S.rk = rank_choose(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
     }
     __syncthreads();
     const int rk = S.rk;

@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(NT, 1) k_hrb_solve(const HrBigProb* probs, int
   if (tid == 0) {
     const int rb = p.st[40 + c];
     const int mp = rows < rb ? rows : rb;
-    S.rk = rank_choose(S.E.lam, mp, *p.tau2, P.rmax, P.ctol, P.rule, P.delta);
+    S.rk = rank_choose(S.E.lam, mp, *p.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
   }
   __syncthreads();
   const int rk = S.rk;

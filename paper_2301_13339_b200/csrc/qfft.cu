@@ -15,8 +15,9 @@
 // K_c = M_c GR_c M_c^H, whose eigenvalues are the squared singular values of
 // the cut-c unfolding and whose eigenvectors are its left singular vectors
 // (the same truncated tensor as LQ + SVD, in exact arithmetic).
-// The doubled cores are never stored: they are formed on the fly from the
-// compact cores (ranks <= RS_XF) kept in shared memory.
+// The doubled cores are never stored: the right-Gram chain runs on the
+// compact cores in block form, and the sweep forms the pushed doubled core
+// on the fly from the compact cores (ranks <= RS_XF) kept in shared memory.
 #include "qtt_kernels.h"
 
 namespace qtt {
@@ -26,9 +27,9 @@ static constexpr int NT = 256;
 // optional phase timing (compile with -DQTT_XF_TIMING): cycles per phase of
 // CTA 0 are accumulated into XfProb::gr scratch tail (debug builds only)
 #ifdef QTT_XF_TIMING
-#define XT_DECL long long xt_t0 = clock64(), xt_acc[6] = {0, 0, 0, 0, 0, 0};
+#define XT_DECL long long xt_t0 = clock64(), xt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #define XT_MARK(k) { long long _t = clock64(); xt_acc[k] += _t - xt_t0; xt_t0 = _t; }
-#define XT_DUMP(ptr) if (threadIdx.x == 0) { for (int _k = 0; _k < 6; ++_k) ((long long*)(ptr))[_k] = xt_acc[_k]; }
+#define XT_DUMP(ptr) if (threadIdx.x == 0) { for (int _k = 0; _k < 8; ++_k) ((long long*)(ptr))[_k] = xt_acc[_k]; }
 #else
 #define XT_DECL
 #define XT_MARK(k)
@@ -67,36 +68,6 @@ template <class SM>
 __device__ __forceinline__ cplx phi_of(const SM& S, const XfParams& P, int q, int a, int t, int be) {
   if (be == 0 || P.axis[q - 1] != a) return cmk(1.0, 0.0);
   return S.phtab[P.bit[q - 1] - t];
-}
-
-// doubled core of position q (p < q <= d) of the current stage into S.D;
-// dims (2 a0) x 2 x (q < d ? 2 b0 : 1)
-template <class SM>
-__device__ void build_doubled(SM& S, const cplx* c, const XfParams& P, int q, int a, int t) {
-  const int d = P.d;
-  const int a0 = S.r[q - 1], b0 = S.r[q];
-  const cplx ph = phi_of(S, P, q, a, t, 1);
-  if (q < d) {
-    const int rows = 2 * a0, cols = 2 * b0;
-    for (int e = threadIdx.x; e < rows * 2 * cols; e += NT) {
-      int i = e % rows, be = (e / rows) & 1, j = e / (2 * rows);
-      cplx v = czero();
-      if (i < a0 && j < b0) v = c[i + a0 * be + 2 * a0 * j];
-      else if (i >= a0 && j >= b0) {
-        v = c[(i - a0) + a0 * be + 2 * a0 * (j - b0)];
-        if (be) v = cmul(ph, v);
-      }
-      S.D[e] = v;
-    }
-  } else {
-    const int rows = 2 * a0;
-    for (int e = threadIdx.x; e < rows * 2; e += NT) {
-      int i = e % rows, be = e / rows;
-      cplx v = (i < a0) ? c[i + a0 * be] : c[(i - a0) + a0 * be];
-      if (i >= a0 && be) v = cmul(ph, v);
-      S.D[e] = v;
-    }
-  }
 }
 
 template <int RSV>
@@ -138,53 +109,77 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       __syncthreads();
       continue;
     }
-    // ---- right Gram chain GR_c, c = d-1 .. p, into global slots
-    build_doubled(S, core(d - 1), P, d, a, t);
-    __syncthreads();
+    // ---- right Gram chain GR_c, c = d-1 .. p, into global slots.  The
+    //      doubled cores blockdiag(C_q, phi_q C_q) (q < d) and vstack(C_d,
+    //      phi_d C_d) with |phi| = 1 give GR_c = [[G_c, H_c^H], [H_c, G_c]]:
+    //        G_{q-1} = sum_be C_q[be] G_q C_q[be]^H       (plain right Gram)
+    //        H_{q-1} = sum_be phi_q(be) C_q[be] H_q C_q[be]^H
+    //      from G_{d-1} = sum_be c_d[be] c_d[be]^H, H_{d-1} = sum_be
+    //      phi_d(be) c_d[be] c_d[be]^H — two r x r chains on the compact
+    //      cores instead of one 2r x 2r chain on materialised doubled cores.
     {
-      const int rows = 2 * S.r[d - 1];
-      for (int e = tid; e < rows * rows; e += NT) {
-        int i = e % rows, j = e / rows;
-        cplx s = czero();
-        for (int be = 0; be < 2; ++be) s = cfma_bc(S.D[i + rows * be], S.D[j + rows * be], s);
-        S.G[0][e] = s;
-        pr.gr[(size_t)(d - 1) * GRS + e] = s;
-      }
-    }
-    __syncthreads();
-    int gc = 0;
-    for (int c = d - 1; c >= p + 1; --c) {
-      build_doubled(S, core(c - 1), P, c, a, t);
-      __syncthreads();
-      const int rows = 2 * S.r[c - 1], cols = 2 * S.r[c];
-      // T[be] = D[be] G   (rows x cols); D is block diagonal (doubled core):
-      // row i < a0 has columns [0, b0), row i >= a0 columns [b0, 2 b0)
-      const int a0c = S.r[c - 1], b0c = S.r[c];
-      const cplx* Gc = S.G[gc];
-      for (int e = tid; e < 2 * rows * cols; e += NT) {
-        int i = e % rows, be = (e / rows) & 1, j = e / (2 * rows);
-        const int l0 = i < a0c ? 0 : b0c;
-        const cplx* Dr = S.D + i + rows * be;
-        S.T[i + rows * j + rows * cols * be] =
-            dot4(l0, l0 + b0c, [&](int l, cplx acc) { return cfma(Dr[2 * rows * l], Gc[l + cols * j], acc); });
+      cplx* SG[2] = {S.G[0], S.G[0] + RS * RS};   // G_c, H_c (ld r_c), generation 0
+      cplx* SN[2] = {S.G[1], S.G[1] + RS * RS};   // generation 1
+      const int a0 = S.r[d - 1];
+      const cplx* c = core(d - 1);
+      const cplx ph = phi_of(S, P, d, a, t, 1);
+      for (int e = tid; e < 2 * a0 * a0; e += NT) {
+        const int w = e / (a0 * a0), ij = e % (a0 * a0), i = ij % a0, j = ij / a0;
+        const cplx s0 = cmul(c[i], cconj(c[j]));
+        const cplx s1 = cmul(c[i + a0], cconj(c[j + a0]));
+        SG[w][i + a0 * j] = w == 0 ? cadd(s0, s1) : cadd(s0, cmul(ph, s1));
       }
       __syncthreads();
-      // Gn = sum_be T[be] D[be]^H (columns of D[j] in the block of row j)
-      for (int e = tid; e < rows * rows; e += NT) {
-        int i = e % rows, j = e / rows;
-        const int l0 = j < a0c ? 0 : b0c;
-        const cplx* T0 = S.T + i;
-        const cplx* T1 = S.T + i + rows * cols;
-        const cplx* D0 = S.D + j;
-        const cplx* D1 = S.D + j + rows;
-        const cplx s = cadd(
-            dot4(l0, l0 + b0c, [&](int l, cplx acc) { return cfma_bc(T0[rows * l], D0[2 * rows * l], acc); }),
-            dot4(l0, l0 + b0c, [&](int l, cplx acc) { return cfma_bc(T1[rows * l], D1[2 * rows * l], acc); }));
-        S.G[gc ^ 1][e] = s;
-        pr.gr[(size_t)(c - 1) * GRS + e] = s;
+      cplx** cur = SG;
+      cplx** nxt = SN;
+      int rc = a0;   // r_c of the chain's current cut c
+      for (int cq = d - 1;; --cq) {
+        // write GR_cq = [[G, H^H], [H, G]] (2 rc x 2 rc) to its slot
+        {
+          const int n2 = 2 * rc;
+          cplx* g = pr.gr + (size_t)cq * GRS;
+          for (int e = tid; e < n2 * n2; e += NT) {
+            const int i = e % n2, j = e / n2;
+            const int bi = i >= rc, bj = j >= rc, ii = i - bi * rc, jj = j - bj * rc;
+            cplx v;
+            if (bi == bj) v = cur[0][ii + rc * jj];
+            else if (bi) v = cur[1][ii + rc * jj];
+            else v = cconj(cur[1][jj + rc * ii]);
+            g[e] = v;
+          }
+        }
+        if (cq <= p) break;
+        // step to cut cq - 1 through core q = cq (compact a1 x 2 x rc)
+        const int q = cq;
+        const int a1 = S.r[q - 1];
+        const cplx* cc = core(q - 1);
+        const cplx phq = phi_of(S, P, q, a, t, 1);
+        cplx* TG = S.D;                       // [w][be]: a1 x rc, ld a1
+        const int tsz = a1 * rc;
+        for (int e = tid; e < 4 * tsz; e += NT) {
+          const int wb = e / tsz, ij = e % tsz, i = ij % a1, j = ij / a1;
+          const int w = wb >> 1, be = wb & 1;
+          const cplx* X = cur[w];
+          const cplx* Cr = cc + i + a1 * be;
+          TG[e] = dotu<RS>(rc, [&](int l, cplx acc) { return cfma(Cr[2 * a1 * l], X[l + rc * j], acc); });
+        }
+        __syncthreads();
+        for (int e = tid; e < 2 * a1 * a1; e += NT) {
+          const int w = e / (a1 * a1), ij = e % (a1 * a1), i = ij % a1, j = ij / a1;
+          const cplx* T0 = TG + (2 * w) * tsz + i;
+          const cplx* T1 = TG + (2 * w + 1) * tsz + i;
+          const cplx* C0 = cc + j;
+          const cplx* C1 = cc + j + a1;
+          const cplx s0 = dotu<RS>(rc, [&](int l, cplx acc) { return cfma_bc(T0[a1 * l], C0[2 * a1 * l], acc); });
+          const cplx s1 = dotu<RS>(rc, [&](int l, cplx acc) { return cfma_bc(T1[a1 * l], C1[2 * a1 * l], acc); });
+          nxt[w][i + a1 * j] = w == 0 ? cadd(s0, s1) : cadd(s0, cmul(phq, s1));
+        }
+        __syncthreads();
+        cplx** tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+        rc = a1;
       }
-      __syncthreads();
-      gc ^= 1;
     }
     XT_MARK(0)
     // ---- rank bounds of the LQ sweep (oracle ROUND_LOCAL (i)): rb_c
@@ -219,7 +214,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         int i = e % rows, j = e / rows;
         const cplx* Er = S.Eb + i;
         const cplx* Gj = S.G[0] + cols * j;
-        S.T[e] = dot4(0, cols, [&](int l, cplx acc) { return cfma(Er[rows * l], Gj[l], acc); });
+        S.T[e] = dotu<R2>(cols, [&](int l, cplx acc) { return cfma(Er[rows * l], Gj[l], acc); });
       }
       __syncthreads();
       // K = T M^H, into the eigensolver of width 16 when rows <= 16 (the
@@ -233,7 +228,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         int i = e % rows, j = e / rows;
         const cplx* Ti = S.T + i;
         const cplx* Ej = S.Eb + j;
-        Kb[i + ldk * j] = dot4(0, cols, [&](int l, cplx acc) { return cfma_bc(Ti[rows * l], Ej[rows * l], acc); });
+        Kb[i + ldk * j] = dotu<R2>(cols, [&](int l, cplx acc) { return cfma_bc(Ti[rows * l], Ej[rows * l], acc); });
       }
       __syncthreads();
       if (c == p) {
@@ -249,11 +244,13 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       XT_MARK(2)
       if (tid == 0) {
         int mp = rows < S.rb[c] ? rows : S.rb[c];
-        S.rk = rank_choose(w16 ? E16.lam : S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta);
+        S.rk = rank_choose(w16 ? E16.lam : S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
       }
       __syncthreads();
+      XT_MARK(6)
       const int rk = S.rk;
       const cplx* U = w16 ? eig_vectors<16, NT>(E16, rows, rk, P.status) : eig_vectors<R2, NT>(S.E, rows, rk, P.status);
+      XT_MARK(7)
       // new core c = U_r  (ap x 2 x rk)
       for (int e = tid; e < rows * rk; e += NT) {
         int i = e % rows, r = e / rows;
@@ -264,7 +261,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         int r = e % rk, l = e / rk;
         const cplx* Ur = U + ldk * r;
         const cplx* El = S.Eb + rows * l;
-        S.Sm[e] = dot4(0, rows, [&](int i, cplx acc) { return cfmac(Ur[i], El[i], acc); });
+        S.Sm[e] = dotu<R2>(rows, [&](int i, cplx acc) { return cfmac(Ur[i], El[i], acc); });
       }
       __syncthreads();
       // next E = Sm * doubled(core c+1)
@@ -276,12 +273,13 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
           const int b1 = S.r[q];
           for (int e = tid; e < rk * 2 * 2 * b1; e += NT) {
             int r = e % rk, be = (e / rk) & 1, j = e / (2 * rk);
-            cplx s = czero();
+            cplx s;
             if (j < b1) {
-              for (int i = 0; i < a1; ++i) s = cfma(S.Sm[r + rk * i], cn[i + a1 * be + 2 * a1 * j], s);
+              s = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * i], cn[i + a1 * be + 2 * a1 * j], acc); });
             } else {
-              for (int i = 0; i < a1; ++i)
-                s = cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be + 2 * a1 * (j - b1)], s);
+              s = dotu<RS>(a1, [&](int i, cplx acc) {
+                return cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be + 2 * a1 * (j - b1)], acc);
+              });
               if (be) s = cmul(phi_of(S, P, q, a, t, 1), s);
             }
             S.Eb[e] = s;
@@ -289,11 +287,8 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         } else {
           for (int e = tid; e < rk * 2; e += NT) {
             int r = e % rk, be = e / rk;
-            cplx s0 = czero(), s1 = czero();
-            for (int i = 0; i < a1; ++i) {
-              s0 = cfma(S.Sm[r + rk * i], cn[i + a1 * be], s0);
-              s1 = cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be], s1);
-            }
+            const cplx s0 = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * i], cn[i + a1 * be], acc); });
+            cplx s1 = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be], acc); });
             if (be) s1 = cmul(phi_of(S, P, q, a, t, 1), s1);
             S.Eb[e] = cadd(s0, s1);
           }

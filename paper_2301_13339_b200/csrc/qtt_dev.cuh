@@ -64,6 +64,22 @@ __device__ __forceinline__ cplx dot4(int l0, int l1, F f) {
   return cadd(cadd(s0, s1), cadd(s2, s3));
 }
 
+// sum_{0 <= l < n} of f(l, acc) for n <= MAXL, fully unrolled with
+// predication: every shared-memory operand is requested up front, so a
+// small dot pays one load latency instead of one per group of terms
+template <int MAXL, class F>
+__device__ __forceinline__ cplx dotu(int n, F f) {
+  cplx s0 = czero(), s1 = czero(), s2 = czero(), s3 = czero();
+#pragma unroll
+  for (int l = 0; l < MAXL; l += 4) {
+    if (l < n) s0 = f(l, s0);
+    if (l + 1 < MAXL && l + 1 < n) s1 = f(l + 1, s1);
+    if (l + 2 < MAXL && l + 2 < n) s2 = f(l + 2, s2);
+    if (l + 3 < MAXL && l + 3 < n) s3 = f(l + 3, s3);
+  }
+  return cadd(cadd(s0, s1), cadd(s2, s3));
+}
+
 // ------------------------------------------------------------ layout maps
 // QTT index q (LSB first) -> element offset in the caller's array.
 //   1D / concat: offset = q (row-major image, x fastest, x bits first).
@@ -107,6 +123,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // ------------------------------------------------------------ status word
 enum { ST_OK = 0, ST_NONFINITE = 1, ST_NOCONV = 2, ST_RANKCAP = 4, ST_FALLBACK = 16 };
 enum { ST_ERRORS = ST_NONFINITE | ST_NOCONV };
+// bytes of the device status buffer reset per call: word 0 = status bits,
+// ints 2-3 / 4-5 = T2 minimum margin / gap (record_min)
+static constexpr size_t STATUS_BYTES = 64;
 __device__ __forceinline__ void raise_status(int* status, int bit) {
   if (status) atomicOr(status, bit);
 }
@@ -197,6 +216,7 @@ struct TridSmem {
   long long tstep[5];        // clock64 per tridiagonalisation sub-phase (diagnostics)
   double anrm;
   int bad;
+  int qready;                // reflectors published to the Q warp (NMAX <= 16 path)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -295,18 +315,27 @@ template <int NMAX, int NT>
 __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x, lane = tid & 31;
-  // ---- normalise by ||A||_F
-  double nrm2 = 0.0;
-  for (int e = tid; e < n * n; e += NT) nrm2 += cabs2(A0[(e % n) + LDA * (e / n)]);
-  nrm2 = block_sum<NT>(nrm2, S.red);
-  const double anrm = sqrt(nrm2);
-  const double inv = anrm > 0.0 ? 1.0 / anrm : 1.0;
-  for (int e = tid; e < n * n; e += NT) {
-    const int i = e % n, j = e / n;
-    A0[i + LDA * j] = cscale(A0[i + LDA * j], inv);
+  double anrm = 0.0;
+  if constexpr (NMAX <= 16) {
+    // the single-warp path normalises in registers and leaves A0 untouched
+    // (it stays the original matrix for a Jacobi fallback); only the Q-warp
+    // counter is reset here
+    if (tid == 0) { S.bad = 0; S.qready = 0; }
+    __syncthreads();
+  } else {
+    // ---- normalise by ||A||_F
+    double nrm2 = 0.0;
+    for (int e = tid; e < n * n; e += NT) nrm2 += cabs2(A0[(e % n) + LDA * (e / n)]);
+    nrm2 = block_sum<NT>(nrm2, S.red);
+    anrm = sqrt(nrm2);
+    const double inv = anrm > 0.0 ? 1.0 / anrm : 1.0;
+    for (int e = tid; e < n * n; e += NT) {
+      const int i = e % n, j = e / n;
+      A0[i + LDA * j] = cscale(A0[i + LDA * j], inv);
+    }
+    if (tid == 0) { S.bad = 0; S.anrm = anrm; S.qready = 0; }
+    __syncthreads();
   }
-  if (tid == 0) { S.bad = 0; S.anrm = anrm; }
-  __syncthreads();
   long long tt0 = clock64();
   // ---- Householder tridiagonalisation by warps 0-3 (named barriers 1/2);
   //      warp 4 accumulates Q = H_0 H_1 ... H_{n-3} explicitly in Qm one step
@@ -319,7 +348,201 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #define TS_MARK(q)
 #endif
   static_assert(NT >= 256, "trid_values needs warps 0-3 (reduction) and 4-7 (Q)");
-  if (wp < 4) {
+  if constexpr (NMAX <= 16) {
+    // ---- n <= 16 (every QTT-FFT / rounding cut at Rhat <= 8): ONE warp
+    //      reduces the whole matrix with no CTA barrier (the four-warp scheme
+    //      below spends ~70% of its time in named barriers).  Lane l keeps row
+    //      i = l & 15 and the columns j = 2t + h (h = l >> 4, t = 0..7) of the
+    //      zero-padded 16 x 16 matrix in registers, so the finished columns
+    //      j <= k of both halves retire together and are skipped statically.
+    //      Per reflector k: column k (x) and k+1 (c) go through smem, y = A x
+    //      from both halves (one xor-16 shuffle), ONE fused reduction (smem,
+    //      one exchange) of |x|^2, Re(x^H y) (half 0) and x^H c (half 1),
+    //      then v, w and the rank-2 update of the live columns.  Warp 1
+    //      (another SM sub-partition) accumulates Q = H_0 ... H_{n-3} one
+    //      reflector behind, released by the counter S.qready.
+    cplx* xs = S.colx;
+    cplx* cs = S.colc;
+    cplx* wsm = S.ypart[1];
+    const int i = lane & 15, h = lane >> 4;
+    if (wp == 0) {
+      cplx a[8];
+      double nr = 0.0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        a[t] = (i < n && 2 * t + h < n) ? A0[i + LDA * (2 * t + h)] : czero();
+        nr += cabs2(a[t]);
+      }
+      nr = warp_sum(nr);
+      const double an = sqrt(nr);
+      const double inv = an > 0.0 ? 1.0 / an : 1.0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) a[t] = cscale(a[t], inv);
+      if (lane == 0) S.anrm = an;
+#ifdef QTT_TRID_TIMING
+      tq = clock64();
+#endif
+      // fully unrolled over k (static register columns, the finished ones
+      // skipped at compile time); a rolled loop with selected columns
+      // measured 1.9x slower despite its smaller code (tools/eig_timing.py)
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+        if (k + 2 >= n) break;
+        const int t0 = (k + 1) >> 1;          // live register columns: t >= t0 (2t + 1 > k)
+        cplx ak = czero(), ak1 = czero();     // a[k >> 1], a[(k + 1) >> 1]
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t == (k >> 1)) ak = a[t];
+          if (t == ((k + 1) >> 1)) ak1 = a[t];
+        }
+        if (h == (k & 1)) xs[i] = (i > k) ? ak : czero();
+        if (h == ((k + 1) & 1)) cs[i] = ak1;
+        __syncwarp();
+        cplx y0 = czero(), y1 = czero();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t >= t0) {
+            if (t & 1) y1 = cfma(a[t], xs[2 * t + h], y1);
+            else y0 = cfma(a[t], xs[2 * t + h], y0);
+          }
+        }
+        cplx yi = cadd(y0, y1);
+        yi.x += __shfl_xor_sync(0xffffffffu, yi.x, 16);
+        yi.y += __shfl_xor_sync(0xffffffffu, yi.y, 16);
+        const cplx xi = xs[i], ci = cs[i];
+        const cplx x0 = xs[k + 1];
+        const double a0 = cs[k + 1].x;
+        const double y0r = __shfl_sync(0xffffffffu, yi.x, k + 1), y0i = __shfl_sync(0xffffffffu, yi.y, k + 1);
+        TS_MARK(0)
+        // half 0: |x|^2, Re(x^H y); half 1: Re, Im of x^H c (4 shuffle levels
+        // within the half, one exchange across)
+        double r1, r2;
+        if (h == 0) {
+          r1 = cabs2(xi);
+          r2 = xi.x * yi.x + xi.y * yi.y;
+        } else {
+          r1 = xi.x * ci.x + xi.y * ci.y;
+          r2 = xi.x * ci.y - xi.y * ci.x;
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+          r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        }
+        const double o1 = __shfl_xor_sync(0xffffffffu, r1, 16), o2 = __shfl_xor_sync(0xffffffffu, r2, 16);
+        const double s2 = h == 0 ? r1 : o1, xAx = h == 0 ? r2 : o2;
+        const cplx xc = h == 0 ? cmk(o1, o2) : cmk(r1, r2);
+        TS_MARK(1)
+        const double x02 = cabs2(x0);
+        // reflect when the column is above 1e-30 ||A|| (below that it is
+        // treated as reduced); the phase of x0 is needed whenever |x0|^2 is a
+        // normal number: tau = 1 / (sig (sig + |x0|)) is only unitary with the
+        // true |x0|
+        const bool refl = s2 > 1e-60;
+        const bool hx0 = x02 > 1e-300;
+        const double rs = drsqrt_nr(refl ? s2 : 1.0);
+        const double r0 = drsqrt_nr(hx0 ? x02 : 1.0);
+        const double sig = s2 * rs;
+        const double ax0 = hx0 ? x02 * r0 : 0.0;
+        const cplx phs = hx0 ? cmk(x0.x * r0, x0.y * r0) : cmk(1.0, 0.0);
+        const cplx beta = cscale(phs, sig);
+        const double tau = refl ? drcp_nr(sig * (sig + ax0)) : 0.0;
+        const cplx vi = (i == k + 1) ? cadd(xi, beta) : xi;
+        const cplx pi = cscale(cfma(beta, ci, yi), tau);
+        // Re(v^H A v) = Re(x^H A x) + Re(beta x^H c) + Re(conj(beta) y_{k+1}) + |beta|^2 a0
+        const double vAv = xAx + (beta.x * xc.x - beta.y * xc.y) + (beta.x * y0r + beta.y * y0i) + cabs2(beta) * a0;
+        const double K = 0.5 * tau * tau * vAv;
+        const cplx wi = refl ? cmk(pi.x - K * vi.x, pi.y - K * vi.y) : czero();
+        cplx* vs = S.hv + LD * k;             // reflector k: the update's v and the Q warp's
+        if (h == 0) {
+          vs[i] = vi;
+          wsm[i] = wi;
+        }
+        __syncwarp();
+        TS_MARK(2)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t >= t0) {
+            const cplx vj = vs[2 * t + h], wj = wsm[2 * t + h];
+            a[t] = csub(a[t], cfma_bc(vi, wj, cmul(wi, cconj(vj))));
+          }
+        }
+        if (lane == 0) {
+          S.tau[k] = tau;
+          S.sub[k] = refl ? cmk(-beta.x, -beta.y) : x0;
+          __threadfence_block();
+          *(volatile int*)&S.qready = k + 1;
+        }
+        TS_MARK(3)
+      }
+#ifdef QTT_TRID_TIMING
+      if (lane == 0)
+        for (int q = 0; q < 4; ++q) S.tstep[q] = ts[q];
+#endif
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int j = 2 * t + h;
+        if (i == j && i < n) S.dg[i] = a[t].x;
+        if (n >= 2 && j == n - 2 && i == n - 1) S.sub[n - 2] = a[t];
+      }
+      __syncwarp();
+      {
+        const int il = lane;
+        const bool hs = il + 1 < n;
+        const cplx al = hs ? S.sub[il] : cmk(1.0, 0.0);
+        const double ab2 = cabs2(al);
+        const double r = ab2 > 1e-60 ? drsqrt_nr(ab2) : 0.0;
+        const double ab = ab2 * r;
+        cplx uu = ab2 > 1e-60 ? cscale(al, r) : cmk(1.0, 0.0);
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const cplx t = make_double2(__shfl_up_sync(0xffffffffu, uu.x, o), __shfl_up_sync(0xffffffffu, uu.y, o));
+          if (il >= o) uu = cmul(t, uu);
+        }
+        if (il == 0) S.ph[0] = cmk(1.0, 0.0);
+        if (hs) {
+          S.ph[il + 1] = uu;
+          S.of[il] = ab;
+          S.e2[il] = ab * ab;
+        }
+      }
+    } else if (wp == 1) {
+      cplx q[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) q[t] = cmk((2 * t + h == i) ? 1.0 : 0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < 14; ++k) {
+        if (k + 2 >= n) break;
+        const int t0 = (k + 1) >> 1;
+        while (*(volatile int*)&S.qready <= k) {
+        }
+        __syncwarp();
+        __threadfence_block();
+        const double tau = S.tau[k];
+        const cplx* v = S.hv + LD * k;
+        cplx s0 = czero(), s1 = czero();
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (t >= t0) {
+            if (t & 1) s1 = cfma(q[t], v[2 * t + h], s1);
+            else s0 = cfma(q[t], v[2 * t + h], s0);
+          }
+        }
+        cplx sq = cadd(s0, s1);
+        sq.x += __shfl_xor_sync(0xffffffffu, sq.x, 16);
+        sq.y += __shfl_xor_sync(0xffffffffu, sq.y, 16);
+        sq = cscale(sq, tau);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t >= t0) q[t] = csub(q[t], cmul(sq, cconj(v[2 * t + h])));
+      }
+      if (i < n) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (2 * t + h < n) Qm[i + LD * (2 * t + h)] = q[t];
+      }
+    }
+  } else if (wp < 4) {
     // Warps 0-3 (one per SM sub-partition, so the FP64 pipes of all four
     // are used): lane i = row i, warp w owns columns j = w + 4t of the
     // zero-padded matrix in registers.  Per step k ONE reduction, done
@@ -556,7 +779,8 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #endif
   }
   __syncthreads();
-  for (int kk = tid; kk < n; kk += NT) lam_out[kk] = S.lam[n - 1 - kk] * anrm;
+  (void)anrm;
+  for (int kk = tid; kk < n; kk += NT) lam_out[kk] = S.lam[n - 1 - kk] * S.anrm;
   if (tid == 0) { long long t = clock64(); S.tph[1] = t - tt0; }
   __syncthreads();
 }
@@ -675,6 +899,23 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, const cplx* Qm,
   __syncthreads();
   if (tid == 0) { long long t = clock64(); S.tph[3] = t - tt0; tt0 = t; }
   if (S.bad) return false;
+  if constexpr (NMAX <= 16) {
+    // ---- back-transformation u = Q (D z), one output element per thread
+    for (int e = tid; e < n * nvec; e += NT) {
+      const int i = e % n, t = e / n;
+      const double* z = S.Z + LD * t;
+      cplx u0 = czero(), u1 = czero();
+#pragma unroll
+      for (int j = 0; j < NMAX; j += 2) {
+        if (j < n) u0 = cfma(Qm[i + LD * j], cscale(S.ph[j], z[j]), u0);
+        if (j + 1 < n) u1 = cfma(Qm[i + LD * (j + 1)], cscale(S.ph[j + 1], z[j + 1]), u1);
+      }
+      U_out[i + LDU * t] = cadd(u0, u1);
+    }
+    __syncthreads();
+    if (tid == 0) S.tph[4] = clock64() - tt0;
+    return true;
+  }
   // ---- back-transformation u = Q D z with the accumulated Q (one output
   //      element per thread)
   for (int e = tid; e < n * nvec; e += NT) {
@@ -1026,6 +1267,12 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
 template <int NMAX, int NT>
 __device__ void eig_values(EigSmem<NMAX>& E, int n) {
   constexpr int LD = NMAX + 1;
+  if constexpr (NMAX <= 16) {
+    // single-warp path: E.A[0] is read, not modified (padding handled in
+    // registers), so it needs no copy for the fallback
+    trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1]);
+    return;
+  }
   for (int e = threadIdx.x; e < NMAX * NMAX; e += NT) {
     const int i = e % NMAX, j = e / NMAX;
     if (i < n && j < n) E.A[1][i + LD * j] = E.A[0][i + LD * j];
@@ -1049,12 +1296,13 @@ __device__ const cplx* eig_vectors(EigSmem<NMAX>& E, int n, int k, int* status) 
     if (threadIdx.x < k) {
       const int t = threadIdx.x;
       double rn = 0.0, an = 0.0;
+      const cplx* Aref = NMAX <= 16 ? E.A[0] : E.A[1];   // the original matrix
       for (int i = 0; i < n; ++i) {
         cplx s = czero();
-        for (int j = 0; j < n; ++j) s = cfma(E.A[1][i + LD * j], E.V[0][j + LD * t], s);
+        for (int j = 0; j < n; ++j) s = cfma(Aref[i + LD * j], E.V[0][j + LD * t], s);
         s = csub(s, cscale(E.V[0][i + LD * t], E.lam[t]));
         rn += cabs2(s);
-        for (int j = 0; j < n; ++j) an += cabs2(E.A[1][i + LD * j]);
+        for (int j = 0; j < n; ++j) an += cabs2(Aref[i + LD * j]);
       }
       if (rn > 1e-20 * an + 1e-300) {
         raise_status(status, NMAX == 16 ? 64 : (NMAX == 20 ? 128 : 256));
@@ -1062,7 +1310,7 @@ __device__ const cplx* eig_vectors(EigSmem<NMAX>& E, int n, int k, int* status) 
           printf("BAD n=%d k=%d t=%d rel=%g\nA=[", n, k, t, sqrt(rn / an));
           for (int i = 0; i < n; ++i) {
             printf("[");
-            for (int j = 0; j < n; ++j) printf("complex(%.17g,%.17g),", E.A[1][i + LD * j].x, E.A[1][i + LD * j].y);
+            for (int j = 0; j < n; ++j) printf("complex(%.17g,%.17g),", Aref[i + LD * j].x, Aref[i + LD * j].y);
             printf("],\n");
           }
           printf("]\nlam=[");
@@ -1075,9 +1323,11 @@ __device__ const cplx* eig_vectors(EigSmem<NMAX>& E, int n, int k, int* status) 
 #endif
     return E.V[0];
   }
-  for (int e = threadIdx.x; e < n * n; e += NT) {
-    const int i = e % n, j = e / n;
-    E.A[0][i + LD * j] = E.A[1][i + LD * j];
+  if constexpr (NMAX > 16) {
+    for (int e = threadIdx.x; e < n * n; e += NT) {
+      const int i = e % n, j = e / n;
+      E.A[0][i + LD * j] = E.A[1][i + LD * j];
+    }
   }
   if (threadIdx.x == 0) {
     E.fallbacks++;
@@ -1098,36 +1348,68 @@ __device__ const cplx* eig_small(EigSmem<NMAX>& E, int n, int k, int* status) {
 }
 
 // --------------------------------------------------------------- RANK rule
+// T2 diagnostics (qtt_report.min_margin / min_gap): the
+// status buffer keeps, at int slots 2-3 and 4-5, the bitwise NOT of the
+// smallest non-negative double seen (0 = none recorded): for non-negative
+// doubles the bit pattern orders like the value, so an atomicMax of ~bits is
+// an order-independent (deterministic) minimum.  Logging only.
+__device__ __forceinline__ void record_min(int* status, int slot, double v) {
+  if (!status || !(v >= 0.0)) return;
+  atomicMax(reinterpret_cast<unsigned long long*>(status + slot), ~(unsigned long long)__double_as_longlong(v));
+}
+
 // lam descending (clamped at 0), m = list length.  See oracle/qtt.py
 // rank_rule: r_tau = min{r : sum_{i>r} lam_i <= tau2}; r = min(r_tau, R);
 // cluster cl(r): r < m, lam_r > 0, lam_r - lam_{r+1} <= ctol * lam_r.
-__device__ __forceinline__ int rank_rule(const double* lam, int m, double tau2, int rmax, double ctol) {
+// With `status`, the decision's tail margin and gap are recorded as the
+// oracle's margin_log defines them: |T - tau2| / tau2 at T(r_tau), T(r_tau-1)
+// (eps decides) or T(R) (the cap decides); (lam_r - lam_{r+1}) / lam_1.
+// Written as short rolled loops: the rule runs once per cut in one thread,
+// where the cost is instruction fetch (a fully unrolled register version
+// measured 4x slower in the transform kernel, ncu stall_no_inst).
+static __device__ __noinline__ int rank_rule(const double* lam, int m, double tau2, int rmax, double ctol,
+                                             int* status = nullptr) {
   if (m <= 0) return 1;
-  double l0 = fmax(lam[0], 0.0);
+  const double l0 = fmax(lam[0], 0.0);
   if (!(l0 > 0.0)) return 1;
-  // tails from the smallest value up
-  double tail = 0.0;
+  // tails from the smallest value up: T(r) for r = m..1, minimal r with
+  // T(r) <= tau2 (T(m) = 0 <= tau2 always; walk down while T(r-1) <= tau2)
+  double tail = 0.0, t_rt = 0.0;
   int r_tau = m;
-  // T(r) for r = m..1: find the minimal r with T(r) <= tau2
-  // T(m) = 0 <= tau2 always; walk down while T(r-1) <= tau2
   for (int r = m; r >= 1; --r) {
     // here tail = T(r)
-    if (tail <= tau2) r_tau = r; else break;
+    if (tail <= tau2) { r_tau = r; t_rt = tail; } else break;
     tail += fmax(lam[r - 1], 0.0);
   }
+  // after the loop: tail = T(r_tau - 1) (T(0) when r_tau = 1)
   int r = r_tau < rmax ? r_tau : rmax;
   auto cl = [&](int q) -> bool {
     if (q >= m) return false;
-    double a = fmax(lam[q - 1], 0.0), b = fmax(lam[q], 0.0);
+    const double a = fmax(lam[q - 1], 0.0), b = fmax(lam[q], 0.0);
     return a > 0.0 && (a - b) <= ctol * a;
   };
   if (cl(r)) {
+    bool up = false;
     if (r_tau <= rmax) {
       int rp = r + 1;
       while (cl(rp)) ++rp;
-      if (rp <= rmax) return rp;
+      if (rp <= rmax) { r = rp; up = true; }
     }
-    while (r > 1 && cl(r)) --r;
+    if (!up)
+      while (r > 1 && cl(r)) --r;
+  }
+  if (status && tau2 > 0.0) {
+    double mg;
+    if (r_tau <= rmax) {
+      mg = fabs(t_rt - tau2);
+      if (r_tau > 1) mg = fmin(mg, fabs(tail - tau2));
+    } else {
+      double tR = 0.0;
+      for (int q = m; q > rmax; --q) tR += fmax(lam[q - 1], 0.0);
+      mg = fabs(tR - tau2);
+    }
+    record_min(status, 2, mg / tau2);
+    if (r < m) record_min(status, 4, (fmax(lam[r - 1], 0.0) - fmax(lam[r], 0.0)) / l0);
   }
   return r;
 }
@@ -1194,8 +1476,8 @@ __device__ __forceinline__ int rank_rule_dropoff(const double* lam, int m, doubl
 
 // rank of a cut under the policy (rule 0: RANK, 1: drop-off)
 __device__ __forceinline__ int rank_choose(const double* lam, int m, double tau2, int rmax, double ctol, int rule,
-                                           double delta) {
-  return rule == 1 ? rank_rule_dropoff(lam, m, delta, rmax, ctol) : rank_rule(lam, m, tau2, rmax, ctol);
+                                           double delta, int* status = nullptr) {
+  return rule == 1 ? rank_rule_dropoff(lam, m, delta, rmax, ctol) : rank_rule(lam, m, tau2, rmax, ctol, status);
 }
 
 }  // namespace qtt

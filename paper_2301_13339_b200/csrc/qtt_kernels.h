@@ -11,6 +11,10 @@ namespace qtt {
 
 // number of kernels launched by this library (bench evidence: gpu_launches)
 void count_launches(int n);
+// pass-level profiling (qtt_profile_enable(2)): CUDA events around the
+// full-array passes, pass = PASS_*, end = 0 before / 1 after the launch
+enum { PASS_LEVEL_GRAM = 0, PASS_PROJECT_X = 1, PASS_PROJECT_W = 2, PASS_EXPAND = 3, PASS_N = 4 };
+void prof_pass(int pass, int end, cudaStream_t st);
 // SMs of the current device (cached per device; grids are sized from it)
 int sm_count();
 

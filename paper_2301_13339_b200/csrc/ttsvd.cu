@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(NT, 1) k_level_solve(const DecProb* probs, int
       eig_values<NE, NT>(S.E, rr);
       if (tid == 0) {
         int mp = rr < (1 << (d - k)) ? rr : (1 << (d - k));
-        S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
+        S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta, prm.status);
       }
       __syncthreads();
       rk = S.rk;
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_solve(const DecProb* probs, int 
 #endif
   if (tid == 0) {
     int mp = rr < (1 << (pr.d - k)) ? rr : (1 << (pr.d - k));
-    S.rk = rank_choose(S.E.lam, mp, *pr.tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
+    S.rk = rank_choose(S.E.lam, mp, *pr.tau2, prm.rmax, prm.ctol, prm.rule, prm.delta, prm.status);
   }
   __syncthreads();
   const int rk = S.rk;
@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(NT, 1) k_finish(const DecProb* probs, int ksta
       eig_values<NE, NT>(S.E, rr);
       if (tid == 0) {
         int mp = rr < n ? rr : n;
-        S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta);
+        S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta, prm.status);
       }
       __syncthreads();
       rk = S.rk;
@@ -1059,7 +1059,9 @@ static std::vector<TtsvdOp> ttsvd_ops(const DecProb* probs_dev, int nprob, int d
   int nsx = 0;
   if (prm.kp > 0 && (1ull << (d - LVL_M)) > (uint64_t)prm.kp) nsx = nblk;
   ops.push_back({true, [=](cudaStream_t st) {
+    prof_pass(PASS_LEVEL_GRAM, 0, st);
     k_level_gram<<<dim3(nblk, nprob), NT, smem_level_gram(), st>>>(probs_dev, nblk, prm.status);
+    prof_pass(PASS_LEVEL_GRAM, 1, st);
     count_launches(1);
     if (nsx) {
       const int need4 = (16 > prm.kp) && ((1ull << (d - 4)) > (uint64_t)prm.kp);
@@ -1072,7 +1074,9 @@ static std::vector<TtsvdOp> ttsvd_ops(const DecProb* probs_dev, int nprob, int d
   int k = LVL_M;
   const int nb = proj_nblk(1 << (d - k), nprob);
   ops.push_back({true, [=](cudaStream_t st) {
+    prof_pass(PASS_PROJECT_X, 0, st);
     k_project<true><<<dim3(nb, nprob), NT, smem_project(), st>>>(probs_dev, k, nb, 1);
+    prof_pass(PASS_PROJECT_X, 1, st);
     count_launches(1);
   }});
   int src_is_a = 1;  // W_m lives in Wa
@@ -1091,8 +1095,11 @@ static std::vector<TtsvdOp> ttsvd_ops(const DecProb* probs_dev, int nprob, int d
       launch_step_solve(probs_dev, nprob, k, prev_nb, prm, st, nsk);
     }});
     const int nb2 = proj_nblk(1 << (d - k), nprob);
+    const bool first_w = k == LVL_M + 1;
     ops.push_back({true, [=](cudaStream_t st) {
+      if (first_w) prof_pass(PASS_PROJECT_W, 0, st);
       k_project<false><<<dim3(nb2, nprob), NT, smem_project(), st>>>(probs_dev, k, nb2, src_is_a);
+      if (first_w) prof_pass(PASS_PROJECT_W, 1, st);
       count_launches(1);
     }});
     src_is_a ^= 1;

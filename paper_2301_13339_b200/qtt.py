@@ -42,7 +42,8 @@ class Report(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int), ("ranks_f", ctypes.c_int * 64), ("ranks_g", ctypes.c_int * 64),
                 ("ranks_fh", ctypes.c_int * 64), ("ranks_gh", ctypes.c_int * 64),
                 ("ranks_z", ctypes.c_int * 64), ("ranks_out", ctypes.c_int * 64),
-                ("ms_total", ctypes.c_float), ("status_bits", ctypes.c_int)]
+                ("ms_total", ctypes.c_float), ("status_bits", ctypes.c_int),
+                ("min_margin", ctypes.c_double), ("min_gap", ctypes.c_double)]
 
 
 class QttError(RuntimeError):
@@ -213,8 +214,10 @@ def qtt_conv_full(f_ptr, g_ptr, y_ptr, shp, dec, fft, shift, scale, ws_ptr, ws_b
         return None
     d = rep.d
     return {"d": d, "ranks_f": list(rep.ranks_f[:d + 1]), "ranks_g": list(rep.ranks_g[:d + 1]),
-            "ranks_out": list(rep.ranks_out[:d + 1]), "ms_total": rep.ms_total,
-            "status_bits": rep.status_bits}
+            "ranks_fh": list(rep.ranks_fh[:d + 1]), "ranks_gh": list(rep.ranks_gh[:d + 1]),
+            "ranks_z": list(rep.ranks_z[:d + 1]), "ranks_out": list(rep.ranks_out[:d + 1]),
+            "ms_total": rep.ms_total, "status_bits": rep.status_bits,
+            "min_margin": rep.min_margin, "min_gap": rep.min_gap}
 
 
 class Comm:
@@ -302,13 +305,22 @@ STAGES = ["ttsvd", "qfft", "hadamard_round", "qifft", "expand"]
 
 
 def qtt_profile_enable(on=True):
-    lib().qtt_profile_enable(1 if on else 0)
+    """on: False/0 off, True/1 stage events, 2 stage + full-array pass events
+    (the decomposition then runs as one chain on the caller's stream)."""
+    lib().qtt_profile_enable(int(on))
+
+
+PASSES = ("pass_level_gram", "pass_project_x", "pass_project_w", "pass_expand")
 
 
 def qtt_profile_read():
-    buf = (ctypes.c_float * 8)()
-    n = lib().qtt_profile_read(buf, 8)
-    return {STAGES[i]: float(buf[i]) for i in range(n)}
+    buf = (ctypes.c_float * 16)()
+    n = lib().qtt_profile_read(buf, 16)
+    out = {STAGES[i]: float(buf[i]) for i in range(min(n, len(STAGES)))}
+    for i in range(len(STAGES), n):
+        if buf[i] >= 0:
+            out[PASSES[i - len(STAGES)]] = float(buf[i])
+    return out
 
 
 def qtt_launch_count():

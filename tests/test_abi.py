@@ -100,3 +100,25 @@ def test_truncation_rule_validation(L):
     assert L.qtt_workspace_bytes(ctypes.byref(shp), ctypes.byref(ok), ctypes.byref(fft), 1) > 0
     for bad in (Q.Trunc(0.0, 10, 1e-10, 1, 0.0), Q.Trunc(0.0, 10, 1e-10, 1, 1.0), Q.Trunc(1e-3, 10, 1e-10, 7, 0.1)):
         assert L.qtt_workspace_bytes(ctypes.byref(shp), ctypes.byref(bad), ctypes.byref(fft), 1) == 0
+
+
+def test_misaligned_inputs_are_rejected_before_device_work(L):
+    """The TT-SVD streams f / g / x with 16-byte copies: a misaligned input
+    or an odd batch stride is QTT_EINVAL, never a sticky device fault
+    (ADVICE r1)."""
+    s = Q.shape(1, [14, 0])
+    dec, fft = Q.trunc(1e-3, 10), Q.trunc(1e-3, 8)
+    nb = L.qtt_workspace_bytes(ctypes.byref(s), ctypes.byref(dec), ctypes.byref(fft), 1)
+    ws = ctypes.c_void_p(1 << 20)
+    ok, bad = ctypes.c_void_p(4096), ctypes.c_void_p(4096 + 8)
+    for f, g in ((bad, ok), (ok, bad)):
+        st = L.qtt_conv_full(f, g, ok, ctypes.byref(s), ctypes.byref(dec), ctypes.byref(fft), None, 1.0,
+                             ws, nb, None, None, None)
+        assert st == Q.QTT_EINVAL and b"16-byte aligned" in L.qtt_last_error()
+    h = ctypes.c_void_p()
+    st = L.qtt_decompose(bad, ctypes.byref(s), ctypes.byref(dec), ws, nb, None, None, ctypes.byref(h))
+    assert st == Q.QTT_EINVAL
+    sb = Q.shape(1, [14, 0], "1d", 2, (1 << 14) + 1, 0, 0)
+    nbb = L.qtt_workspace_bytes(ctypes.byref(sb), ctypes.byref(dec), ctypes.byref(fft), 1)
+    st = L.qtt_decompose(ok, ctypes.byref(sb), ctypes.byref(dec), ws, nbb, None, None, ctypes.byref(h))
+    assert st == Q.QTT_EINVAL and b"stride must be even" in L.qtt_last_error()

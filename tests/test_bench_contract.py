@@ -34,7 +34,7 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_our_arm_line():
-    d = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline"])
+    d = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--config", "c2", "--extra", "none"])
     assert BASE <= set(d)
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0
     assert d["dtype"] == "f64" and "workload" in d["config"] and "l2" in d["config"]
@@ -46,3 +46,12 @@ def test_our_arm_line():
     assert r["achieved"] > 0 and "traffic" in r
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["status_bits"] & 3 == 0
+    # per-pass HBM evidence of the full-array kernels
+    for k in ("pass_level_gram", "pass_project_x", "pass_project_w", "pass_expand"):
+        assert d["hbm_passes"][k]["alg_GBps"] > 0
+    assert d["t2"]["min_margin"] > 0
+    # both arms describe the workload with the identical config dict
+    ref = _run(["--impl", "reference", "--config", "c2", "--steps", "1", "--warmup", "1",
+                "--ref-step-seconds", "1"])
+    assert ref["config"] == d["config"]
+    assert ref["metric"] == d["metric"] and ref["unit"] == d["unit"] and ref["scaling"] == d["scaling"]
