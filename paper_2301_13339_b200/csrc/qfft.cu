@@ -202,21 +202,35 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       }
     }
     __syncthreads();
-    // ---- truncation sweep, c = p .. d-1
+    // ---- truncation sweep, c = p .. d-1.  GR_c comes from the L2-resident
+    //      slots through a cp.async double buffer: GR_{c+1} is requested
+    //      right after cut c's T = M GR_c and lands during its eigensolve.
     int ap = S.r[p - 1];
+    {
+      const int cols = 2 * S.r[p];
+      for (int e = tid; e < cols * cols; e += NT) cp_async16(&S.G[0][e], &pr.gr[(size_t)p * GRS + e]);
+      cp_async_commit();
+    }
     for (int c = p; c <= d - 1; ++c) {
       const int rows = 2 * ap, cols = 2 * S.r[c];
+      const int gb = (c - p) & 1;
       XT_MARK(5)
-      for (int e = tid; e < cols * cols; e += NT) S.G[0][e] = pr.gr[(size_t)c * GRS + e];
+      cp_async_wait<0>();
       __syncthreads();
       // T = M G  (rows x cols), M = Eb (ld rows)
       for (int e = tid; e < rows * cols; e += NT) {
         int i = e % rows, j = e / rows;
         const cplx* Er = S.Eb + i;
-        const cplx* Gj = S.G[0] + cols * j;
+        const cplx* Gj = S.G[gb] + cols * j;
         S.T[e] = dotu<R2>(cols, [&](int l, cplx acc) { return cfma(Er[rows * l], Gj[l], acc); });
       }
       __syncthreads();
+      if (c + 1 <= d - 1) {
+        const int cols1 = 2 * S.r[c + 1];
+        for (int e = tid; e < cols1 * cols1; e += NT)
+          cp_async16(&S.G[gb ^ 1][e], &pr.gr[(size_t)(c + 1) * GRS + e]);
+      }
+      cp_async_commit();
       // K = T M^H, into the eigensolver of width 16 when rows <= 16 (the
       // steady state at Rhat <= 8; 18% fewer cycles than width R2 at n = 16,
       // tools/dev_trid_timing.py), else width R2; both share S.E's memory
@@ -295,8 +309,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         }
       }
       __syncthreads();
-      if (tid == 0) S.r[c] = rk;
-      __syncthreads();
+      if (tid == 0) S.r[c] = rk;   // read next after the barrier at the top of cut c+1
       ap = rk;
       XT_MARK(3)
     }

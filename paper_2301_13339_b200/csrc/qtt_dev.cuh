@@ -216,7 +216,6 @@ struct TridSmem {
   long long tstep[5];        // clock64 per tridiagonalisation sub-phase (diagnostics)
   double anrm;
   int bad;
-  int qready;                // reflectors published to the Q warp (NMAX <= 16 path)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -318,9 +317,8 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   double anrm = 0.0;
   if constexpr (NMAX <= 16) {
     // the single-warp path normalises in registers and leaves A0 untouched
-    // (it stays the original matrix for a Jacobi fallback); only the Q-warp
-    // counter is reset here
-    if (tid == 0) { S.bad = 0; S.qready = 0; }
+    // (it stays the original matrix for a Jacobi fallback)
+    if (tid == 0) S.bad = 0;
     __syncthreads();
   } else {
     // ---- normalise by ||A||_F
@@ -333,7 +331,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       const int i = e % n, j = e / n;
       A0[i + LDA * j] = cscale(A0[i + LDA * j], inv);
     }
-    if (tid == 0) { S.bad = 0; S.anrm = anrm; S.qready = 0; }
+    if (tid == 0) { S.bad = 0; S.anrm = anrm; }
     __syncthreads();
   }
   long long tt0 = clock64();
@@ -360,7 +358,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     //      one exchange) of |x|^2, Re(x^H y) (half 0) and x^H c (half 1),
     //      then v, w and the rank-2 update of the live columns.  Warp 1
     //      (another SM sub-partition) accumulates Q = H_0 ... H_{n-3} one
-    //      reflector behind, released by the counter S.qready.
+    //      reflector behind, handed over through named barriers 1 / 2.
     cplx* xs = S.colx;
     cplx* cs = S.colc;
     cplx* wsm = S.ypart[1];
@@ -458,7 +456,16 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
           vs[i] = vi;
           wsm[i] = wi;
         }
+        if (lane == 0) {
+          S.tau[k] = tau;
+          S.sub[k] = refl ? cmk(-beta.x, -beta.y) : x0;
+        }
         __syncwarp();
+        // hand reflector k to the Q warp: named barrier 1 ("full", release
+        // of the stores above); barrier 2 ("empty") keeps warp 0 at most one
+        // reflector ahead so the two barriers' phases stay paired
+        if (k > 0) asm volatile("bar.sync 2, 64;" ::: "memory");
+        asm volatile("bar.arrive 1, 64;" ::: "memory");
         TS_MARK(2)
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
@@ -466,12 +473,6 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
             const cplx vj = vs[2 * t + h], wj = wsm[2 * t + h];
             a[t] = csub(a[t], cfma_bc(vi, wj, cmul(wi, cconj(vj))));
           }
-        }
-        if (lane == 0) {
-          S.tau[k] = tau;
-          S.sub[k] = refl ? cmk(-beta.x, -beta.y) : x0;
-          __threadfence_block();
-          *(volatile int*)&S.qready = k + 1;
         }
         TS_MARK(3)
       }
@@ -514,10 +515,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       for (int k = 0; k < 14; ++k) {
         if (k + 2 >= n) break;
         const int t0 = (k + 1) >> 1;
-        while (*(volatile int*)&S.qready <= k) {
-        }
-        __syncwarp();
-        __threadfence_block();
+        asm volatile("bar.sync 1, 64;" ::: "memory");     // reflector k published
         const double tau = S.tau[k];
         const cplx* v = S.hv + LD * k;
         cplx s0 = czero(), s1 = czero();
@@ -535,6 +533,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #pragma unroll
         for (int t = 0; t < 8; ++t)
           if (t >= t0) q[t] = csub(q[t], cmul(sq, cconj(v[2 * t + h])));
+        if (k + 3 < n) asm volatile("bar.arrive 2, 64;" ::: "memory");
       }
       if (i < n) {
 #pragma unroll
@@ -753,7 +752,6 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     const int k = tid / gl, j = tid % gl;
     const int steps = gl == 32 ? 11 : (gl == 16 ? 13 : 17);
     const double sj = (double)(j + 1) / (double)(gl + 1);
-    const double inv_g1 = 1.0 / (double)(gl + 1);
     double l = lo, h = hi;
     const int base = (tid & 31) & ~(gl - 1);
     const unsigned gmask = (gl == 32) ? 0xffffffffu : (((1u << gl) - 1u) << base);
@@ -767,11 +765,12 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       }
       const unsigned bal = __ballot_sync(0xffffffffu, c >= k + 1) & gmask;
       const int first = bal ? (__ffs(bal) - 1 - base) : gl;
-      const double w = h - l;
-      const double nh = (first < gl) ? l + w * (double)(first + 1) * inv_g1 : h;
-      const double nl = (first > 0) ? l + w * (double)first * inv_g1 : l;
-      l = nl;
-      h = nh;
+      // the new bracket ends are the group's evaluated points x_{first-1},
+      // x_first, taken by shuffle (no int -> double conversion on the chain)
+      const double xh = __shfl_sync(0xffffffffu, x, base + (first < gl ? first : gl - 1));
+      const double xl = __shfl_sync(0xffffffffu, x, base + (first > 0 ? first - 1 : 0));
+      h = (first < gl) ? xh : h;
+      l = (first > 0) ? xl : l;
     }
     if (k < n && j == 0) S.lam[k] = 0.5 * (l + h);
 #ifdef QTT_TRID_TIMING
@@ -785,13 +784,20 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   __syncthreads();
 }
 
-template <int NMAX, int NT>
-__device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, const cplx* Qm, cplx* U_out, int LDU) {
+// nspec vectors of T are formed speculatively while thread NT-1 runs side()
+// (the truncations decide their rank there, off the critical path); the
+// count actually kept is then read from *nvec_smem (<= nspec) after the
+// first barrier.  nvec_smem == nullptr: all nspec vectors.
+template <int NMAX, int NT, class Side>
+__device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nvec_smem, Side side, const cplx* Qm,
+                             cplx* U_out, int LDU) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   long long tt0 = clock64();
+  static_assert(NT > 32, "the side task runs in the last warp");
+  if (tid == NT - 1) side();
   // ---- eigenvectors of T (division-free twisted factorisation), one thread each
-  if (tid < nvec) {
+  if (tid < nspec) {
     const int k = n - 1 - tid;
     const double lam = S.lam[k];
     double P[NMAX + 1], Qd[NMAX + 2];
@@ -869,6 +875,7 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, const cplx* Qm,
     if (!(nz > 0.0)) S.bad = 1;
   }
   __syncthreads();
+  const int nvec = nvec_smem ? (*nvec_smem < nspec ? *nvec_smem : nspec) : nspec;
   if (tid == 0) { long long t = clock64(); S.tph[2] = t - tt0; tt0 = t; }
   // ---- re-orthogonalise clusters (normalised eigenvalues within 1e-4):
   //      modified Gram-Schmidt by warp 0, lane = component (n <= 32)
@@ -933,6 +940,11 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, const cplx* Qm,
   __syncthreads();
   if (tid == 0) S.tph[4] = clock64() - tt0;
   return true;
+}
+
+template <int NMAX, int NT>
+__device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nvec, const cplx* Qm, cplx* U_out, int LDU) {
+  return trid_vectors<NMAX, NT>(S, n, nvec, nullptr, [] {}, Qm, U_out, LDU);
 }
 
 template <int NMAX>
@@ -1285,12 +1297,28 @@ __device__ void eig_values(EigSmem<NMAX>& E, int n) {
 #ifdef QTT_EIG_CHECK
 __device__ int g_eig_dumped = 0;
 #endif
+// eig_vectors with the rank decided concurrently: side() (run by one thread
+// of the last warp) must write the kept count (1 <= k <= kspec) to *k_smem;
+// vectors of the kspec largest eigenvalues are formed meanwhile.
+template <int NMAX, int NT, class Side>
+__device__ const cplx* eig_vectors_spec(EigSmem<NMAX>& E, int n, int kspec, const int* k_smem, Side side,
+                                        int* status);
+
 template <int NMAX, int NT>
 __device__ const cplx* eig_vectors(EigSmem<NMAX>& E, int n, int k, int* status) {
+  return eig_vectors_spec<NMAX, NT>(E, n, k, nullptr, [] {}, status);
+}
+
+template <int NMAX, int NT, class Side>
+__device__ const cplx* eig_vectors_spec(EigSmem<NMAX>& E, int n, int kspec, const int* k_smem, Side side,
+                                        int* status) {
   constexpr int LD = NMAX + 1;
-  if (k > n) k = n;
+  if (kspec > n) kspec = n;
+  if (kspec < 1) kspec = 1;
+  const bool ok = trid_vectors<NMAX, NT>(E.u.tr, n, kspec, k_smem, side, E.V[1], E.V[0], LD);
+  int k = k_smem ? (*k_smem < kspec ? *k_smem : kspec) : kspec;
   if (k < 1) k = 1;
-  if (trid_vectors<NMAX, NT>(E.u.tr, n, k, E.V[1], E.V[0], LD)) {
+  if (ok) {
 #ifdef QTT_EIG_CHECK
     // debug builds: residual of every returned pair against the original matrix
     if (threadIdx.x < k) {
