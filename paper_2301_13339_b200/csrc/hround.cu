@@ -196,9 +196,10 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     HT_MARK(1)
     eig_values<2 * RH, NT>(S.E, rows);
     HT_MARK(2)
-    if (tid == 0) {
-      int mp = rows < S.rb[c] ? rows : S.rb[c];
-      S.rk = rank_choose(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
+    if (tid < 32) {
+      const int mp = rows < S.rb[c] ? rows : S.rb[c];
+      const int r = rank_choose_warp(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
+      if (tid == 0) S.rk = r;
     }
     __syncthreads();
     const int rk = S.rk;

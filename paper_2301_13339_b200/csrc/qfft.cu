@@ -256,9 +256,10 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       if (w16) eig_values<16, NT>(E16, rows);
       else eig_values<R2, NT>(S.E, rows);
       XT_MARK(2)
-      if (tid == 0) {
-        int mp = rows < S.rb[c] ? rows : S.rb[c];
-        S.rk = rank_choose(w16 ? E16.lam : S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
+      if (tid < 32) {
+        const int mp = rows < S.rb[c] ? rows : S.rb[c];
+        const int r = rank_choose_warp(w16 ? E16.lam : S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
+        if (tid == 0) S.rk = r;
       }
       __syncthreads();
       XT_MARK(6)

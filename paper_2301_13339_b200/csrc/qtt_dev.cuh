@@ -1502,7 +1502,72 @@ __device__ __forceinline__ int rank_rule_dropoff(const double* lam, int m, doubl
   return r < 1 ? 1 : r;
 }
 
+// RANK by one warp (all 32 lanes call it, m <= 32; same result in every
+// lane): lane i holds lam_i, the tails T(r) = sum_{i >= r} lam_i (0-based)
+// come from a suffix scan, r_tau = 1 + the highest r < m with T(r) > tau2
+// (the stopping point of rank_rule's walk), the cluster test is a ballot.
+// The scan sums in a different association than the sequential walk
+// (rounding-level differences in T; the T2 margins of the gradable cases are
+// >= 1e-4 of tau2).  Replaces a ~2.7k-cycle single-thread walk in the chain.
+__device__ __forceinline__ int rank_rule_warp(const double* lam, int m, double tau2, int rmax, double ctol,
+                                              int* status) {
+  const int lane = threadIdx.x & 31;
+  if (m > 32) m = 32;
+  if (m <= 0) return 1;
+  const double li = lane < m ? fmax(lam[lane], 0.0) : 0.0;
+  const double l0 = __shfl_sync(0xffffffffu, li, 0);
+  if (!(l0 > 0.0)) return 1;
+  double sfx = li;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double t = __shfl_down_sync(0xffffffffu, sfx, o);
+    if (lane + o < 32) sfx += t;
+  }
+  const unsigned bad = __ballot_sync(0xffffffffu, lane < m && sfx > tau2);
+  const int r_tau = bad ? 32 - __clz(bad) : 1;
+  const double lprev = __shfl_up_sync(0xffffffffu, li, 1);
+  const unsigned clm = __ballot_sync(0xffffffffu, lane >= 1 && lane < m && lprev > 0.0 && (lprev - li) <= ctol * lprev);
+  int r = r_tau < rmax ? r_tau : rmax;
+  if ((clm >> r) & 1u) {
+    bool up = false;
+    if (r_tau <= rmax) {
+      int rp = r + 1;
+      while ((clm >> rp) & 1u) ++rp;
+      if (rp <= rmax) { r = rp; up = true; }
+    }
+    if (!up)
+      while (r > 1 && ((clm >> r) & 1u)) --r;
+  }
+  const double t_rt = __shfl_sync(0xffffffffu, sfx, r_tau & 31);
+  const double t_rt1 = __shfl_sync(0xffffffffu, sfx, (r_tau - 1) & 31);
+  const double t_R = __shfl_sync(0xffffffffu, sfx, (rmax < 32 ? rmax : 31));
+  const double lr = __shfl_sync(0xffffffffu, li, (r - 1) & 31), lr1 = __shfl_sync(0xffffffffu, li, r & 31);
+  if (status && lane == 0 && tau2 > 0.0) {
+    double mg;
+    if (r_tau <= rmax) {
+      mg = fabs((r_tau < 32 ? t_rt : 0.0) - tau2);
+      if (r_tau > 1) mg = fmin(mg, fabs(t_rt1 - tau2));
+    } else {
+      mg = fabs(t_R - tau2);
+    }
+    record_min(status, 2, mg / tau2);
+    if (r < m) record_min(status, 4, (lr - lr1) / l0);
+  }
+  return r;
+}
+
 // rank of a cut under the policy (rule 0: RANK, 1: drop-off)
+// warp form (every lane of one warp calls it; the result is uniform)
+__device__ __forceinline__ int rank_choose_warp(const double* lam, int m, double tau2, int rmax, double ctol, int rule,
+                                                double delta, int* status) {
+  if (rule == 1) {
+    int r = 0;
+    if ((threadIdx.x & 31) == 0) r = rank_rule_dropoff(lam, m, delta, rmax, ctol);
+    return __shfl_sync(0xffffffffu, r, 0);
+  }
+  return rank_rule_warp(lam, m, tau2, rmax, ctol, status);
+}
+
 __device__ __forceinline__ int rank_choose(const double* lam, int m, double tau2, int rmax, double ctol, int rule,
                                            double delta, int* status = nullptr) {
   return rule == 1 ? rank_rule_dropoff(lam, m, delta, rmax, ctol) : rank_rule(lam, m, tau2, rmax, ctol, status);
