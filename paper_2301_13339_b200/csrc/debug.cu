@@ -20,7 +20,13 @@ __global__ void __launch_bounds__(NT, 1) k_debug_eigh(const cplx* A, int n, doub
     for (int e = threadIdx.x; e < n * n; e += NT) E.A[0][(e % n) + LD * (e / n)] = A[e];
     __syncthreads();
     if (mode == 1) V = jacobi_eig<NMAX, NT>(E, n, nullptr);
-    else V = eig_small<NMAX, NT>(E, n, mode >= 2 ? mode - 1 : n, nullptr);
+    else if (mode >= 64) {
+      // diagnostics (tools/eig_timing.py --warm): the vector phase twice on
+      // the same T, phase cycles of the second (instruction-cache warm) run
+      eig_values<NMAX, NT>(E, n);
+      V = eig_vectors<NMAX, NT>(E, n, mode - 64, nullptr);
+      V = eig_vectors<NMAX, NT>(E, n, mode - 64, nullptr);
+    } else V = eig_small<NMAX, NT>(E, n, mode >= 2 ? mode - 1 : n, nullptr);
   }
   for (int e = threadIdx.x; e < n * n; e += NT) U[e] = V[(e % n) + LD * (e / n)];
   for (int i = threadIdx.x; i < n; i += NT) lam[i] = E.lam[i];

@@ -311,7 +311,8 @@ __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const doubl
 }
 
 template <int NMAX, int NT>
-__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm) {
+__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm,
+                            bool real_in = false) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x, lane = tid & 31;
   double anrm = 0.0;
@@ -541,7 +542,136 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
           if (2 * t + h < n) Qm[i + LD * (2 * t + h)] = q[t];
       }
     }
-  } else if (wp < 4) {
+  } else {
+  bool done = false;
+  if constexpr (NMAX <= 20) {
+    if (real_in) {
+      done = true;
+      // ---- real symmetric A, n <= 20 (every TT-SVD step Gram at R_max <= 10:
+      //      the unfoldings are real): ONE warp, lane i = row i with all
+      //      NMAX columns of the (normalised, zero-padded) matrix in
+      //      registers, real reflectors, no CTA barrier; per step one fused
+      //      reduction of |x|^2, x.y, x.c (y = A x, c = column k+1, the same
+      //      algebra as the complex paths); warp 1 accumulates Q one
+      //      reflector behind through named barriers 1 / 2.  A quarter of
+      //      the complex arithmetic of the four-warp scheme below.
+      double* xr = reinterpret_cast<double*>(S.colx);
+      double* cr = reinterpret_cast<double*>(S.colc);
+      double* vr = reinterpret_cast<double*>(S.ypart[0]);
+      double* wr = reinterpret_cast<double*>(S.ypart[1]);
+      double* hr = reinterpret_cast<double*>(S.hv);     // reflector k at hr[LD k + i]
+      const int i = lane;
+      const bool live = i < NMAX;
+      if (wp == 0) {
+        double a[NMAX];
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) a[j] = live ? A0[i + LDA * j].x : 0.0;
+#pragma unroll
+        for (int k = 0; k + 2 < NMAX; ++k) {
+          if (k + 2 >= n) break;
+          xr[i] = (i > k) ? a[k] : 0.0;
+          cr[i] = a[k + 1];
+          __syncwarp();
+          double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+          for (int j = k + 1; j < NMAX; ++j) {
+            if ((j - k) & 1) y0 = fma(a[j], xr[j], y0);
+            else y1 = fma(a[j], xr[j], y1);
+          }
+          const double yi = y0 + y1;
+          const double xi = xr[i], ci = cr[i];
+          const double x0 = xr[k + 1], a0 = cr[k + 1];
+          double r1 = xi * xi, r2 = xi * yi, r3 = xi * ci;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            r1 += __shfl_xor_sync(0xffffffffu, r1, o);
+            r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+            r3 += __shfl_xor_sync(0xffffffffu, r3, o);
+          }
+          const double y0k = __shfl_sync(0xffffffffu, yi, k + 1);
+          const double s2 = r1, xAx = r2, xc = r3;
+          const bool refl = s2 > 1e-60;
+          const double rs = drsqrt_nr(refl ? s2 : 1.0);
+          const double sig = s2 * rs;
+          const double ax0 = fabs(x0);
+          const double beta = x0 < 0.0 ? -sig : sig;
+          const double tau = refl ? drcp_nr(sig * (sig + ax0)) : 0.0;
+          const double vi = (i == k + 1) ? xi + beta : xi;
+          const double pi = tau * fma(beta, ci, yi);
+          // v^T A v = x^T A x + 2 beta x.c + beta^2 a0 with x.c = c.x = y_{k+1}
+          // taken from the reduction (the Gram is symmetric only to rounding)
+          const double vAv = xAx + beta * xc + beta * y0k + beta * beta * a0;
+          const double K = 0.5 * tau * tau * vAv;
+          const double wi = refl ? fma(-K, vi, pi) : 0.0;
+          if (live) {
+            vr[i] = vi;
+            wr[i] = wi;
+            hr[LD * k + i] = vi;
+          }
+          if (lane == 0) {
+            S.tau[k] = tau;
+            S.sub[k] = refl ? cmk(-beta, 0.0) : cmk(x0, 0.0);
+          }
+          __syncwarp();
+          if (k > 0) asm volatile("bar.sync 2, 64;" ::: "memory");
+          asm volatile("bar.arrive 1, 64;" ::: "memory");
+#pragma unroll
+          for (int j = k + 1; j < NMAX; ++j) a[j] = fma(-vi, wr[j], fma(-wi, vr[j], a[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) {
+          if (i == j && i < n) S.dg[i] = a[j];
+          if (n >= 2 && j == n - 2 && i == n - 1) S.sub[n - 2] = cmk(a[j], 0.0);
+        }
+        __syncwarp();
+        {
+          const bool hs = i + 1 < n;
+          const double al = hs ? S.sub[i].x : 1.0;
+          const double ab = fabs(al);
+          double u = (al < 0.0) ? -1.0 : 1.0;   // phase of alpha_i (real: a sign)
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, u, o);
+            if (i >= o) u *= t;
+          }
+          if (i == 0) S.ph[0] = cmk(1.0, 0.0);
+          if (hs) {
+            S.ph[i + 1] = cmk(u, 0.0);
+            S.of[i] = ab;
+            S.e2[i] = ab * ab;
+          }
+        }
+      } else if (wp == 1) {
+        double q[NMAX];
+#pragma unroll
+        for (int j = 0; j < NMAX; ++j) q[j] = (j == i) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k + 2 < NMAX; ++k) {
+          if (k + 2 >= n) break;
+          asm volatile("bar.sync 1, 64;" ::: "memory");
+          const double tau = S.tau[k];
+          const double* v = hr + LD * k;
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int j = k + 1; j < NMAX; ++j) {
+            if ((j - k) & 1) s0 = fma(q[j], v[j], s0);
+            else s1 = fma(q[j], v[j], s1);
+          }
+          const double sq = tau * (s0 + s1);
+#pragma unroll
+          for (int j = k + 1; j < NMAX; ++j) q[j] = fma(-sq, v[j], q[j]);
+          if (k + 3 < n) asm volatile("bar.arrive 2, 64;" ::: "memory");
+        }
+        if (live && i < n) {
+#pragma unroll
+          for (int j = 0; j < NMAX; ++j)
+            if (j < n) Qm[i + LD * j] = cmk(q[j], 0.0);
+        }
+      }
+    }
+  }
+  if (!done) {
+  if (wp < 4) {
     // Warps 0-3 (one per SM sub-partition, so the FP64 pipes of all four
     // are used): lane i = row i, warp w owns columns j = w + 4t of the
     // zero-padded matrix in registers.  Per step k ONE reduction, done
@@ -732,6 +862,8 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       }
     }
   }
+  }   // !done
+  }   // NMAX > 16
   __syncthreads();
   if (tid == 0) { long long t = clock64(); S.tph[0] = t - tt0; tt0 = t; }
   // ---- eigenvalues by multisection
@@ -1277,7 +1409,7 @@ __device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
 // Tridiagonal solver first; Jacobi (whole problem again) if it reports a
 // dependent cluster (status bit ST_FALLBACK).
 template <int NMAX, int NT>
-__device__ void eig_values(EigSmem<NMAX>& E, int n) {
+__device__ void eig_values(EigSmem<NMAX>& E, int n, bool real_in = false) {
   constexpr int LD = NMAX + 1;
   if constexpr (NMAX <= 16) {
     // single-warp path: E.A[0] is read, not modified (padding handled in
@@ -1291,7 +1423,7 @@ __device__ void eig_values(EigSmem<NMAX>& E, int n) {
     else E.A[0][i + LD * j] = czero();   // the tridiagonalisation runs on the zero-padded matrix
   }
   __syncthreads();
-  trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1]);
+  trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1], real_in);
 }
 
 #ifdef QTT_EIG_CHECK

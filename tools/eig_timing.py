@@ -29,13 +29,13 @@ def graded(n, seed, decades=8.0):
     return 0.5 * (A + A.conj().T)
 
 
-def run(A, nvec, w20=False, reps=20):
+def run(A, nvec, w20=False, reps=20, warm=False):
     n = A.shape[0]
     a = torch.from_numpy(np.ascontiguousarray(A.T).view(np.float64).copy()).cuda()
     lam = torch.empty(n, dtype=torch.float64, device="cuda")
     U = torch.empty(2 * n * n, dtype=torch.float64, device="cuda")
     sw = torch.zeros(16, dtype=torch.int32, device="cuda")
-    mode = (2 + nvec) | (256 if w20 else 0)
+    mode = ((64 + nvec) if warm else (2 + nvec)) | (256 if w20 else 0)
     Q.qtt_debug_eigh(a.data_ptr(), n, lam.data_ptr(), U.data_ptr(), sw.data_ptr(),
                      torch.cuda.current_stream().cuda_stream, mode=mode, reps=reps)
     torch.cuda.synchronize()
@@ -51,6 +51,9 @@ def main(ns):
             nvec = min(8, n)
             for _ in range(2):       # warm
                 lg, ug, sw = run(A, nvec, w20)
+            if "--warm" in sys.argv:
+                _, _, sw2 = run(A, nvec, w20, warm=True)
+                print(f"   second vector pass: {dict(zip(PHASES[2:], sw2[4:7].tolist()))}")
             lw = np.linalg.eigvalsh(A)[::-1]
             el = np.max(np.abs(lg - lw)) / np.abs(lw[0])
             res = np.linalg.norm(A @ ug[:, :nvec] - ug[:, :nvec] * lg[:nvec]) / np.linalg.norm(A)
@@ -63,4 +66,4 @@ def main(ns):
 
 
 if __name__ == "__main__":
-    main([int(x) for x in sys.argv[1:]] or [8, 12, 16, 20])
+    main([int(x) for x in sys.argv[1:] if x.isdigit()] or [8, 12, 16, 20])
