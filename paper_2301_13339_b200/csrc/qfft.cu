@@ -217,12 +217,14 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       XT_MARK(5)
       cp_async_wait<0>();
       __syncthreads();
-      // T = M G  (rows x cols), M = Eb (ld rows)
-      for (int e = tid; e < rows * cols; e += NT) {
-        int i = e % rows, j = e / rows;
-        const cplx* Er = S.Eb + i;
-        const cplx* Gj = S.G[gb] + cols * j;
-        S.T[e] = dotu<R2>(cols, [&](int l, cplx acc) { return cfma(Er[rows * l], Gj[l], acc); });
+      // T = M G  (rows x cols), M = Eb (ld rows); DMMA tiles
+      {
+        const cplx* Gm = S.G[gb];
+        cgemm_dmma<NT / 32>(
+            rows, cols, cols,
+            [&](int i, int l) { return (i < rows && l < cols) ? S.Eb[i + rows * l] : czero(); },
+            [&](int l, int j) { return (l < cols && j < cols) ? Gm[l + cols * j] : czero(); },
+            [&](int i, int j, cplx v) { if (i < rows && j < cols) S.T[i + rows * j] = v; });
       }
       __syncthreads();
       if (c + 1 <= d - 1) {
@@ -238,12 +240,12 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       EigSmem<16>& E16 = *reinterpret_cast<EigSmem<16>*>(&S.E);
       cplx* Kb = w16 ? E16.A[0] : S.E.A[0];
       const int ldk = w16 ? EigSmem<16>::LD : LD;
-      for (int e = tid; e < rows * rows; e += NT) {
-        int i = e % rows, j = e / rows;
-        const cplx* Ti = S.T + i;
-        const cplx* Ej = S.Eb + j;
-        Kb[i + ldk * j] = dotu<R2>(cols, [&](int l, cplx acc) { return cfma_bc(Ti[rows * l], Ej[rows * l], acc); });
-      }
+      // K = T M^H (rows x rows); DMMA tiles
+      cgemm_dmma<NT / 32>(
+          rows, rows, cols,
+          [&](int i, int l) { return (i < rows && l < cols) ? S.T[i + rows * l] : czero(); },
+          [&](int l, int j) { return (l < cols && j < rows) ? cconj(S.Eb[j + rows * l]) : czero(); },
+          [&](int i, int j, cplx v) { if (i < rows && j < rows) Kb[i + ldk * j] = v; });
       __syncthreads();
       if (c == p) {
         double tr = 0.0;
@@ -271,13 +273,12 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         int i = e % rows, r = e / rows;
         core(c - 1)[i + rows * r] = U[i + ldk * r];
       }
-      // Sm = U_r^H M  (rk x cols)
-      for (int e = tid; e < rk * cols; e += NT) {
-        int r = e % rk, l = e / rk;
-        const cplx* Ur = U + ldk * r;
-        const cplx* El = S.Eb + rows * l;
-        S.Sm[e] = dotu<R2>(rows, [&](int i, cplx acc) { return cfmac(Ur[i], El[i], acc); });
-      }
+      // Sm = U_r^H M  (rk x cols); DMMA tiles
+      cgemm_dmma<NT / 32>(
+          rk, cols, rows,
+          [&](int r, int i) { return (r < rk && i < rows) ? cconj(U[i + ldk * r]) : czero(); },
+          [&](int i, int l) { return (i < rows && l < cols) ? S.Eb[i + rows * l] : czero(); },
+          [&](int r, int l, cplx v) { if (r < rk && l < cols) S.Sm[r + rk * l] = v; });
       __syncthreads();
       // next E = Sm * doubled(core c+1)
       {

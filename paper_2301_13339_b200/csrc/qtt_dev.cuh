@@ -111,6 +111,37 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
+// Small complex product C (M x N) = A (M x K) . B (K x N) on the FP64 tensor
+// cores, for the per-cut products of the truncation sweeps (M, N, K <= 32).
+// fa(i, k), fb(k, j) return the operands (zero outside the matrix: callers
+// predicate their shared-memory loads), fc(i, j, v) stores.  Each 8 x 8 output
+// tile is one warp's job: per k-chunk of 4 one (re, im) load of each operand
+// and four DMMA m8n8k4 (Re += ar br - ai bi, Im += ar bi + ai br).  Replaces
+// one-output-per-thread dots whose two 16-byte shared loads per complex FMA
+// made these phases shared-memory bound.
+template <int NWARPS, class FA, class FB, class FC>
+__device__ __forceinline__ void cgemm_dmma(int M, int N, int K, FA fa, FB fb, FC fc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, nk = (K + 3) >> 2;
+  const int ar = lane >> 2, ac = lane & 3;     // A fragment (row, k); B fragment (k, col) = (ac, ar)
+  for (int t = w; t < tm * tn; t += NWARPS) {
+    const int ti = t % tm, tj = t / tm;
+    double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int k = 4 * kc + ac;
+      const cplx a = fa(8 * ti + ar, k);
+      const cplx b = fb(k, 8 * tj + ar);
+      dmma884(r0, r1, a.x, b.x);
+      dmma884(r0, r1, -a.y, b.y);
+      dmma884(i0, i1, a.x, b.y);
+      dmma884(i0, i1, a.y, b.x);
+    }
+    const int ci = 8 * ti + ar, cj = 8 * tj + 2 * ac;
+    fc(ci, cj, cmk(r0, i0));
+    fc(ci, cj + 1, cmk(r1, i1));
+  }
+}
+
 // ---------------------------------------------------------- cp.async
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
