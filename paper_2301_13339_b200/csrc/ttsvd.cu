@@ -63,6 +63,27 @@ __device__ __forceinline__ void load_chunk_async(double* sm, const double* x, ui
   }
 }
 
+// TMA (bulk-copy) form of load_chunk_async, issued by one warp: the 64 rows
+// of 512 B of an interleaved 64 x 64 tile, or the 128 columns of 256 B of a
+// 1D / concat chunk, land in the same padded smem layout; the 32 KB are
+// counted on the stage's mbarrier.
+__device__ __forceinline__ void load_chunk_bulk(double* sm, const double* x, uint64_t c, int layout, int bx,
+                                                uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) mbar_expect_tx(bar, CH * sizeof(double));
+  __syncwarp();
+  if (layout == LAYOUT_INTERLEAVED) {
+    const uint64_t q0 = c * (uint64_t)CH;
+    const uint64_t x0 = compact_even(q0), y0 = compact_even(q0 >> 1);
+    for (int row = lane; row < 64; row += 32)
+      bulk_g2s(sm + row * SLD, x + ((y0 + row) << bx) + x0, 64 * sizeof(double), bar);
+  } else {
+    const double* src = x + c * (uint64_t)CH;
+    for (int col = lane; col < CH / 32; col += 32)
+      bulk_g2s(sm + col * S1D, src + 32 * col, 32 * sizeof(double), bar);
+  }
+}
+
 // ------------------------------------------------- DMMA Gram accumulation
 // acc[pair][2] += Gram contributions of a (nrows x 4) column step, rows split
 // in 8-row blocks nb <= 4, unique block pairs (bi <= bj).
@@ -121,6 +142,69 @@ __device__ void gram_reduce_cta(const double (&acc)[10][2], double* scratch, dou
 }
 
 // ------------------------------------------------------------------- K1
+#ifdef QTT_LEVEL_GRAM_TMA
+// A/B variant (diagnostic build -DQTT_LEVEL_GRAM_TMA): the chunks stream
+// through a 3-stage ring filled by TMA bulk copies (warp 0 issues one
+// 512-byte copy per tile row, an mbarrier per stage counts the bytes).
+// Measured slower than the cp.async double buffer below (C4 level-1 Gram
+// pass 1.18 vs 0.86 ms, 56% vs 76% of HBM; profiles/r02_summary.md), so the
+// product build keeps cp.async.
+static constexpr int LG_STAGES = 3;
+__global__ void __launch_bounds__(NT) k_level_gram(const DecProb* probs, int nblk, int* status) {
+  const DecProb& pr = probs[blockIdx.y];
+  extern __shared__ double smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + LG_STAGES * CHUNK_SMEM);
+  const uint64_t nchunks = 1ull << (pr.dl - 12);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  double acc[10][2];
+#pragma unroll
+  for (int i = 0; i < 10; ++i) acc[i][0] = acc[i][1] = 0.0;
+  int rowoff[4];
+#pragma unroll
+  for (int b = 0; b < 4; ++b) rowoff[b] = chunk_off(8 * b + (lane >> 2), pr.layout);
+  bool bad = false;
+  if (tid == 0) {
+    for (int st = 0; st < LG_STAGES; ++st) mbar_init(&bars[st], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const uint64_t c0 = blockIdx.x;
+  if (w == 0) {
+    for (int st = 0; st < LG_STAGES - 1; ++st) {
+      const uint64_t cc = c0 + (uint64_t)st * nblk;
+      if (cc < nchunks) load_chunk_bulk(smem + st * CHUNK_SMEM, pr.x, cc, pr.layout, pr.bx, &bars[st]);
+    }
+  }
+  int it = 0;
+  for (uint64_t c = c0; c < nchunks; c += nblk, ++it) {
+    const int st = it % LG_STAGES;
+    // refill the stage consumed in the previous iteration (every thread
+    // passed that iteration's closing barrier)
+    if (w == 0) {
+      const uint64_t cn = c + (uint64_t)(LG_STAGES - 1) * nblk;
+      const int sn = (it + LG_STAGES - 1) % LG_STAGES;
+      if (cn < nchunks) load_chunk_bulk(smem + sn * CHUNK_SMEM, pr.x, cn, pr.layout, pr.bx, &bars[sn]);
+    }
+    mbar_wait(&bars[st], (unsigned)((it / LG_STAGES) & 1));
+    const double* s = smem + st * CHUNK_SMEM;
+    // 32 k-steps of 4 columns per chunk, 4 per warp
+#pragma unroll
+    for (int kk = 0; kk < CH_COLS / 4 / (NT / 32); ++kk) {
+      int ks = w * (CH_COLS / 4 / (NT / 32)) + kk;
+      int col = 4 * ks + (lane & 3);
+      int coff = chunk_off((uint32_t)col << LVL_M, pr.layout);
+      double a[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        a[b] = s[rowoff[b] + coff];
+        bad |= !isfinite(a[b]);
+      }
+      gram_step(acc, a, 4);
+    }
+    __syncthreads();
+  }
+#else
+static constexpr int LG_STAGES = 2;
 __global__ void __launch_bounds__(NT) k_level_gram(const DecProb* probs, int nblk, int* status) {
   const DecProb& pr = probs[blockIdx.y];
   extern __shared__ double smem[];
@@ -163,6 +247,7 @@ __global__ void __launch_bounds__(NT) k_level_gram(const DecProb* probs, int nbl
   }
   cp_async_wait<0>();
   __syncthreads();
+#endif
   if (bad) raise_status(status, ST_NONFINITE);
   double* out = pr.part + (size_t)blockIdx.x * 1024;
   gram_reduce_cta(acc, smem, out);
@@ -871,7 +956,7 @@ __global__ void __launch_bounds__(NT, 1) k_finish(const DecProb* probs, int ksta
   if (tid == 0) pr.ranks[d] = 1;
 }
 
-size_t smem_level_gram() { return 2 * CHUNK_SMEM * sizeof(double); }
+size_t smem_level_gram() { return LG_STAGES * CHUNK_SMEM * sizeof(double) + LG_STAGES * sizeof(uint64_t); }
 template <int NE> size_t smem_level_solve() { return sizeof(LevelSolveSmem<NE>); }
 size_t smem_project() { return sizeof(ProjSmem); }
 template <int NE> size_t smem_step_solve() { return sizeof(StepSolveSmem<NE>); }
