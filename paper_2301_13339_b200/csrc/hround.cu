@@ -40,6 +40,7 @@ struct HrSmem {
   int rf[MAXD + 1], rg[MAXD + 1], r[MAXD + 1], rb[MAXD + 1];
   int rk;
   double tau2;
+  double mdefer[4];   // deferred T2 record of the last RANK (margins_flush)
 };
 
 __device__ void load_core(cplx* dst, const cplx* src, int n) {
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
   const int tid = threadIdx.x;
   const int d = P.d;
   for (int q = tid; q <= d; q += NT) { S.rf[q] = pr.f_ranks[q]; S.rg[q] = pr.g_ranks[q]; }
+  if (tid == 0) S.mdefer[1] = 0.0;
   __syncthreads();
   // ---------------- right Gram chain (unless launch_hr_gr_chain computed it
   //                  with the mode products spread over the GPU)
@@ -198,12 +200,13 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     HT_MARK(2)
     if (tid < 32) {
       const int mp = rows < S.rb[c] ? rows : S.rb[c];
-      const int r = rank_choose_warp(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
+      const int r = rank_choose_warp(S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status, S.mdefer);
       if (tid == 0) S.rk = r;
     }
     __syncthreads();
+    auto flush = [&] { if ((tid & 31) == 0) margins_flush(S.mdefer, P.status); };
+    const cplx* U = eig_vectors_spec<2 * RH, NT>(S.E, rows, S.rk, nullptr, flush, P.status);
     const int rk = S.rk;
-    const cplx* U = eig_vectors<2 * RH, NT>(S.E, rows, rk, P.status);
     cplx* oc = pr.out_cores + (size_t)(c - 1) * SLOT;
     for (int e = tid; e < rows * rk; e += NT) {
       int i = e % rows, r = e / rows;

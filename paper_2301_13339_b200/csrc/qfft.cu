@@ -53,6 +53,7 @@ struct XfBufs {
   int rb[MAXD + 1];
   int rk;
   double tau2;
+  double mdefer[4];          // deferred T2 record of the last RANK (margins_flush)
 };
 template <int RSV, bool SMEM_CORES = (RSV <= 10)>
 struct XfSmem : XfBufs<RSV> {
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
   // load (conj for the inverse); twiddle table
   for (int q = tid; q <= d; q += NT) S.r[q] = pr.in_ranks[q];
   if (tid < 32) S.phtab[tid] = tid == 0 ? cmk(1.0, 0.0) : cexpipi(-ldexp(1.0, -tid));
+  if (tid == 0) S.mdefer[1] = 0.0;
   __syncthreads();
   for (int q = 0; q < d; ++q) {
     const int n = S.r[q] * 2 * S.r[q + 1];
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
             g[e] = v;
           }
         }
+        XT_MARK(4)
         if (cq <= p) break;
         // step to cut cq - 1 through core q = cq (compact a1 x 2 x rc)
         const int q = cq;
@@ -164,6 +167,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
           TG[e] = dotu<RS>(rc, [&](int l, cplx acc) { return cfma(Cr[2 * a1 * l], X[l + rc * j], acc); });
         }
         __syncthreads();
+        XT_MARK(0)
         for (int e = tid; e < 2 * a1 * a1; e += NT) {
           const int w = e / (a1 * a1), ij = e % (a1 * a1), i = ij % a1, j = ij / a1;
           const cplx* T0 = TG + (2 * w) * tsz + i;
@@ -175,6 +179,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
           nxt[w][i + a1 * j] = w == 0 ? cadd(s0, s1) : cadd(s0, cmul(phq, s1));
         }
         __syncthreads();
+        XT_MARK(0)
         cplx** tmp = cur;
         cur = nxt;
         nxt = tmp;
@@ -258,15 +263,19 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       if (w16) eig_values<16, NT>(E16, rows);
       else eig_values<R2, NT>(S.E, rows);
       XT_MARK(2)
+      // RANK (its T2 record deferred to the last warp during the vectors)
       if (tid < 32) {
         const int mp = rows < S.rb[c] ? rows : S.rb[c];
-        const int r = rank_choose_warp(w16 ? E16.lam : S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status);
+        const int r = rank_choose_warp(w16 ? E16.lam : S.E.lam, mp, S.tau2, P.rmax, P.ctol, P.rule, P.delta, P.status,
+                                       S.mdefer);
         if (tid == 0) S.rk = r;
       }
       __syncthreads();
       XT_MARK(6)
+      auto flush = [&] { if ((tid & 31) == 0) margins_flush(S.mdefer, P.status); };
+      const cplx* U = w16 ? eig_vectors_spec<16, NT>(E16, rows, S.rk, nullptr, flush, P.status)
+                          : eig_vectors_spec<R2, NT>(S.E, rows, S.rk, nullptr, flush, P.status);
       const int rk = S.rk;
-      const cplx* U = w16 ? eig_vectors<16, NT>(E16, rows, rk, P.status) : eig_vectors<R2, NT>(S.E, rows, rk, P.status);
       XT_MARK(7)
       // new core c = U_r  (ap x 2 x rk)
       for (int e = tid; e < rows * rk; e += NT) {

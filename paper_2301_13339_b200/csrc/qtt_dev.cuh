@@ -366,6 +366,14 @@ __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const doubl
   return cnt;
 }
 
+// the reflector loops of the single-warp tridiagonalisations: fully unrolled
+// (static register columns) or rolled (small code: the one-CTA solve kernels
+// run cold, instruction-fetch bound)
+#ifdef QTT_TRID_ROLLED
+#define TRID_KLOOP _Pragma("unroll 1")
+#else
+#define TRID_KLOOP _Pragma("unroll")
+#endif
 template <int NMAX, int NT>
 __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm,
                             bool real_in = false) {
@@ -437,21 +445,17 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
 #ifdef QTT_TRID_TIMING
       tq = clock64();
 #endif
-      // fully unrolled over k (static register columns, the finished ones
-      // skipped at compile time); a rolled loop with selected columns
-      // measured 1.9x slower despite its smaller code (tools/eig_timing.py)
-#pragma unroll
+      // unrolled over k (static register columns, the finished ones skipped
+      // at compile time) unless QTT_TRID_ROLLED
+      // columns 0 (x of step 0, below the diagonal) and 1 (c of step 0) to
+      // smem; later steps get theirs from the update of the step before
+      // (predicated stores: no register array is ever indexed by k)
+      if (h == 0) xs[i] = (i > 0) ? a[0] : czero();
+      else cs[i] = a[0];
+      TRID_KLOOP
       for (int k = 0; k < 14; ++k) {
         if (k + 2 >= n) break;
         const int t0 = (k + 1) >> 1;          // live register columns: t >= t0 (2t + 1 > k)
-        cplx ak = czero(), ak1 = czero();     // a[k >> 1], a[(k + 1) >> 1]
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if (t == (k >> 1)) ak = a[t];
-          if (t == ((k + 1) >> 1)) ak1 = a[t];
-        }
-        if (h == (k & 1)) xs[i] = (i > k) ? ak : czero();
-        if (h == ((k + 1) & 1)) cs[i] = ak1;
         __syncwarp();
         cplx y0 = czero(), y1 = czero();
 #pragma unroll
@@ -529,6 +533,9 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
           if (t >= t0) {
             const cplx vj = vs[2 * t + h], wj = wsm[2 * t + h];
             a[t] = csub(a[t], cfma_bc(vi, wj, cmul(wi, cconj(vj))));
+            // next step's x (column k+1 below row k+1) and c (column k+2)
+            if (2 * t + h == k + 1) xs[i] = (i > k + 1) ? a[t] : czero();
+            if (2 * t + h == k + 2) cs[i] = a[t];
           }
         }
         TS_MARK(3)
@@ -568,7 +575,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       cplx q[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) q[t] = cmk((2 * t + h == i) ? 1.0 : 0.0, 0.0);
-#pragma unroll
+      TRID_KLOOP
       for (int k = 0; k < 14; ++k) {
         if (k + 2 >= n) break;
         const int t0 = (k + 1) >> 1;
@@ -622,17 +629,19 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
         double a[NMAX];
 #pragma unroll
         for (int j = 0; j < NMAX; ++j) a[j] = live ? A0[i + LDA * j].x : 0.0;
-#pragma unroll
+        xr[i] = (i > 0) ? a[0] : 0.0;     // step 0's x and c; later ones from the update
+        cr[i] = a[1];
+        TRID_KLOOP
         for (int k = 0; k + 2 < NMAX; ++k) {
           if (k + 2 >= n) break;
-          xr[i] = (i > k) ? a[k] : 0.0;
-          cr[i] = a[k + 1];
           __syncwarp();
           double y0 = 0.0, y1 = 0.0;
 #pragma unroll
-          for (int j = k + 1; j < NMAX; ++j) {
-            if ((j - k) & 1) y0 = fma(a[j], xr[j], y0);
-            else y1 = fma(a[j], xr[j], y1);
+          for (int j = 0; j < NMAX; ++j) {
+            if (j > k) {
+              if (j & 1) y0 = fma(a[j], xr[j], y0);
+              else y1 = fma(a[j], xr[j], y1);
+            }
           }
           const double yi = y0 + y1;
           const double xi = xr[i], ci = cr[i];
@@ -672,7 +681,13 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
           if (k > 0) asm volatile("bar.sync 2, 64;" ::: "memory");
           asm volatile("bar.arrive 1, 64;" ::: "memory");
 #pragma unroll
-          for (int j = k + 1; j < NMAX; ++j) a[j] = fma(-vi, wr[j], fma(-wi, vr[j], a[j]));
+          for (int j = 0; j < NMAX; ++j) {
+            if (j > k) {
+              a[j] = fma(-vi, wr[j], fma(-wi, vr[j], a[j]));
+              if (j == k + 1) xr[i] = (i > k + 1) ? a[j] : 0.0;
+              if (j == k + 2) cr[i] = a[j];
+            }
+          }
         }
 #pragma unroll
         for (int j = 0; j < NMAX; ++j) {
@@ -701,7 +716,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
         double q[NMAX];
 #pragma unroll
         for (int j = 0; j < NMAX; ++j) q[j] = (j == i) ? 1.0 : 0.0;
-#pragma unroll
+        TRID_KLOOP
         for (int k = 0; k + 2 < NMAX; ++k) {
           if (k + 2 >= n) break;
           asm volatile("bar.sync 1, 64;" ::: "memory");
@@ -709,13 +724,16 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
           const double* v = hr + LD * k;
           double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int j = k + 1; j < NMAX; ++j) {
-            if ((j - k) & 1) s0 = fma(q[j], v[j], s0);
-            else s1 = fma(q[j], v[j], s1);
+          for (int j = 0; j < NMAX; ++j) {
+            if (j > k) {
+              if (j & 1) s0 = fma(q[j], v[j], s0);
+              else s1 = fma(q[j], v[j], s1);
+            }
           }
           const double sq = tau * (s0 + s1);
 #pragma unroll
-          for (int j = k + 1; j < NMAX; ++j) q[j] = fma(-sq, v[j], q[j]);
+          for (int j = 0; j < NMAX; ++j)
+            if (j > k) q[j] = fma(-sq, v[j], q[j]);
           if (k + 3 < n) asm volatile("bar.arrive 2, 64;" ::: "memory");
         }
         if (live && i < n) {
@@ -972,10 +990,11 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   __syncthreads();
 }
 
-// nspec vectors of T are formed speculatively while thread NT-1 runs side()
-// (the truncations decide their rank there, off the critical path); the
-// count actually kept is then read from *nvec_smem (<= nspec) after the
-// first barrier.  nvec_smem == nullptr: all nspec vectors.
+// nspec vectors of T are formed speculatively (warp 0) while the last warp
+// runs side() — every lane of it calls side(): the truncations decide their
+// rank there with the warp-level RANK, off the critical path; the count
+// actually kept is then read from *nvec_smem (<= nspec) after the first
+// barrier.  nvec_smem == nullptr: all nspec vectors.
 template <int NMAX, int NT, class Side>
 __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nvec_smem, Side side, const cplx* Qm,
                              cplx* U_out, int LDU) {
@@ -983,7 +1002,7 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
   long long tt0 = clock64();
   static_assert(NT > 32, "the side task runs in the last warp");
-  if (tid == NT - 1) side();
+  if (wp == NT / 32 - 1) side();
   // ---- eigenvectors of T (division-free twisted factorisation), one thread each
   if (tid < nspec) {
     const int k = n - 1 - tid;
@@ -1069,7 +1088,9 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
   //      modified Gram-Schmidt by warp 0, lane = component (n <= 32)
   if (tid < 32) {
     const int i = tid;
-    int c0 = 0;
+    // no two kept eigenvalues within 1e-4: nothing to re-orthogonalise
+    const bool near = i + 1 < nvec && S.lam[n - 1 - i] - S.lam[n - 2 - i] <= 1e-4;
+    int c0 = __ballot_sync(0xffffffffu, near) ? 0 : nvec;
     while (c0 < nvec) {
       int c1 = c0 + 1;
       while (c1 < nvec && S.lam[n - 1 - (c1 - 1)] - S.lam[n - 1 - c1] <= 1e-4) ++c1;
@@ -1485,7 +1506,7 @@ __device__ void eig_values(EigSmem<NMAX>& E, int n, bool real_in = false) {
 #ifdef QTT_EIG_CHECK
 __device__ int g_eig_dumped = 0;
 #endif
-// eig_vectors with the rank decided concurrently: side() (run by one thread
+// eig_vectors with the rank decided concurrently: side() (run by every lane
 // of the last warp) must write the kept count (1 <= k <= kspec) to *k_smem;
 // vectors of the kspec largest eigenvalues are formed meanwhile.
 template <int NMAX, int NT, class Side>
@@ -1698,7 +1719,7 @@ __device__ __forceinline__ int rank_rule_dropoff(const double* lam, int m, doubl
 // (rounding-level differences in T; the T2 margins of the gradable cases are
 // >= 1e-4 of tau2).  Replaces a ~2.7k-cycle single-thread walk in the chain.
 __device__ __forceinline__ int rank_rule_warp(const double* lam, int m, double tau2, int rmax, double ctol,
-                                              int* status) {
+                                              int* status, double* defer = nullptr) {
   const int lane = threadIdx.x & 31;
   if (m > 32) m = 32;
   if (m <= 0) return 1;
@@ -1738,22 +1759,39 @@ __device__ __forceinline__ int rank_rule_warp(const double* lam, int m, double t
     } else {
       mg = fabs(t_R - tau2);
     }
-    record_min(status, 2, mg / tau2);
-    if (r < m) record_min(status, 4, (lr - lr1) / l0);
+    const double gp = r < m ? lr - lr1 : -1.0;
+    if (defer) {
+      // recorded later by margins_flush, off the chain's critical path
+      defer[0] = mg;
+      defer[1] = tau2;
+      defer[2] = gp;
+      defer[3] = l0;
+    } else {
+      record_min(status, 2, mg / tau2);
+      if (gp >= 0.0) record_min(status, 4, gp / l0);
+    }
   }
   return r;
+}
+// the T2 record deferred by rank_rule_warp (one thread; defer[1] = tau2 > 0
+// marks a pending record, cleared here)
+__device__ __forceinline__ void margins_flush(double* defer, int* status) {
+  if (!status || !(defer[1] > 0.0)) return;
+  record_min(status, 2, defer[0] / defer[1]);
+  if (defer[2] >= 0.0) record_min(status, 4, defer[2] / defer[3]);
+  defer[1] = 0.0;
 }
 
 // rank of a cut under the policy (rule 0: RANK, 1: drop-off)
 // warp form (every lane of one warp calls it; the result is uniform)
 __device__ __forceinline__ int rank_choose_warp(const double* lam, int m, double tau2, int rmax, double ctol, int rule,
-                                                double delta, int* status) {
+                                                double delta, int* status, double* defer = nullptr) {
   if (rule == 1) {
     int r = 0;
     if ((threadIdx.x & 31) == 0) r = rank_rule_dropoff(lam, m, delta, rmax, ctol);
     return __shfl_sync(0xffffffffu, r, 0);
   }
-  return rank_rule_warp(lam, m, tau2, rmax, ctol, status);
+  return rank_rule_warp(lam, m, tau2, rmax, ctol, status, defer);
 }
 
 __device__ __forceinline__ int rank_choose(const double* lam, int m, double tau2, int rmax, double ctol, int rule,

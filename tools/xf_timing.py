@@ -25,7 +25,7 @@ from paper_2301_13339_b200 import qtt as Q  # noqa: E402
 from paper_2301_13339_b200 import synth  # noqa: E402
 from gpu_util import gpu_decompose, stream, ws  # noqa: E402
 
-NAMES = ["GR chain", "K formation", "eig values", "push", "tail", "cut start", "rank", "vectors"]
+NAMES = ["GR chain (products)", "K formation", "eig values", "push", "GR write", "cut start", "rank", "vectors"]
 
 
 def run(x, label, eps=1e-3, rhat=8):
