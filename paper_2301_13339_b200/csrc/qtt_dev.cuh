@@ -272,6 +272,7 @@ struct TridSmem {
   long long tstep[5];        // clock64 per tridiagonalisation sub-phase (diagnostics)
   double anrm;
   int bad;
+  unsigned zbad;             // twisted vectors that came out zero (underflow): inverse iteration
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -383,7 +384,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   if constexpr (NMAX <= 16) {
     // the single-warp path normalises in registers and leaves A0 untouched
     // (it stays the original matrix for a Jacobi fallback)
-    if (tid == 0) S.bad = 0;
+    if (tid == 0) { S.bad = 0; S.zbad = 0u; }
     __syncthreads();
   } else {
     // ---- normalise by ||A||_F
@@ -396,7 +397,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       const int i = e % n, j = e / n;
       A0[i + LDA * j] = cscale(A0[i + LDA * j], inv);
     }
-    if (tid == 0) { S.bad = 0; S.anrm = anrm; }
+    if (tid == 0) { S.bad = 0; S.zbad = 0u; S.anrm = anrm; }
     __syncthreads();
   }
   long long tt0 = clock64();
@@ -990,6 +991,103 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   __syncthreads();
 }
 
+// Replacement for a numerically dependent cluster vector a of T (called by
+// warp 0, lane i = component): three steps of inverse iteration
+// y = (T - lam_a I)^{-1} x (Thomas recurrence by lane 0, pivots kept away
+// from zero at 1e-15 ||T||), each preceded by Gram-Schmidt against the
+// vectors 0..a-1 kept so far; returns the orthogonalised, unnormalised
+// result (the caller checks its norm).  Scratch: S.red (x / y), S.tau (c').
+template <int NMAX>
+__device__ __noinline__ double inverse_iter_vec(TridSmem<NMAX>& S, int n, int a, int i) {
+  constexpr int LD = NMAX + 1;
+  const double sg = S.lam[n - 1 - a];
+  double za = (i < n) ? sin(0.7 * i + 1.3 * a + 0.1) : 0.0;
+  auto orth = [&] {
+    for (int b = 0; b < a; ++b) {
+      const double zb = (i < n) ? S.Z[LD * b + i] : 0.0;
+      za -= warp_sum(zb * za) * zb;
+    }
+  };
+  for (int it = 0; it < 3; ++it) {
+    orth();
+    const double nz = warp_sum(za * za);
+    za = nz > 0.0 ? za * (1.0 / sqrt(nz)) : za;
+    if (i < n) S.red[i] = za;
+    __syncwarp();
+    if (i == 0) {
+      double* x = S.red;
+      double* cp = S.tau;
+      auto piv = [](double m) { return fabs(m) < 1e-15 ? (m < 0.0 ? -1e-15 : 1e-15) : m; };
+      double m = piv(S.dg[0] - sg);
+      cp[0] = n > 1 ? S.of[0] / m : 0.0;
+      x[0] = x[0] / m;
+      for (int k = 1; k < n; ++k) {
+        m = piv((S.dg[k] - sg) - S.of[k - 1] * cp[k - 1]);
+        cp[k] = k + 1 < n ? S.of[k] / m : 0.0;
+        x[k] = (x[k] - S.of[k - 1] * x[k - 1]) / m;
+      }
+      for (int k = n - 2; k >= 0; --k) x[k] -= cp[k] * x[k + 1];
+    }
+    __syncwarp();
+    za = (i < n) ? S.red[i] : 0.0;
+    __syncwarp();
+  }
+  const double nz = warp_sum(za * za);
+  za = nz > 0.0 ? za * (1.0 / sqrt(nz)) : za;
+  orth();
+  return za;
+}
+
+// The twisted factorisation of T - lam I in ratio form, for the vectors whose
+// division-free determinants left the floating-point range:
+// D+_i = (d_i - lam) - e_{i-1}^2 / D+_{i-1}, D-_i = (d_i - lam) - e_i^2 / D-_{i+1},
+// twist r at the (jc+1)-th smallest |gamma_i| = |D+_i + D-_i - (d_i - lam)|,
+// z_r = 1, z_i = -(e_i / D+_i) z_{i+1} (i < r), z_i = -(e_{i-1} / D-_i) z_{i-1}
+// (i > r); pivots kept off zero.  Writes the unnormalised z (n entries) to
+// z_out, returns |z|^2.  One thread, out of line (rare path).
+template <int NMAX>
+__device__ __noinline__ double twisted_ratio(TridSmem<NMAX>& S, int n, double lam, int jc, double* z_out) {
+  // D+ / D- in this thread's slice of the (now free) Householder-vector
+  // storage: no local-memory arrays
+  constexpr int LD = NMAX + 1;
+  double* Dp = reinterpret_cast<double*>(S.hv) + (size_t)(threadIdx.x & 31) * 2 * LD;
+  double* Dm = Dp + LD;
+  auto safe = [](double v) { return fabs(v) < 1e-280 ? (v < 0.0 ? -1e-280 : 1e-280) : v; };
+  Dp[0] = safe(S.dg[0] - lam);
+  for (int i = 1; i < n; ++i) Dp[i] = safe((S.dg[i] - lam) - S.e2[i - 1] / Dp[i - 1]);
+  Dm[n - 1] = safe(S.dg[n - 1] - lam);
+  for (int i = n - 2; i >= 0; --i) Dm[i] = safe((S.dg[i] - lam) - S.e2[i] / Dm[i + 1]);
+  int r = 0;
+  double prev = -1.0;
+  int prev_r = -1;
+  for (int rep = 0; rep <= jc; ++rep) {
+    double best = 1e308;
+    int rb = 0;
+    for (int i = 0; i < n; ++i) {
+      const double v = fabs(Dp[i] + Dm[i] - (S.dg[i] - lam));
+      const bool above = (v > prev) || (v == prev && i > prev_r);
+      if (above && v < best) { best = v; rb = i; }
+    }
+    prev = best;
+    prev_r = rb;
+    r = rb;
+  }
+  double nz = 1.0, zr = 1.0;
+  z_out[r] = 1.0;
+  for (int i = r - 1; i >= 0; --i) {
+    zr = -S.of[i] / Dp[i] * zr;
+    z_out[i] = zr;
+    nz = fma(zr, zr, nz);
+  }
+  zr = 1.0;
+  for (int i = r + 1; i < n; ++i) {
+    zr = -S.of[i - 1] / Dm[i] * zr;
+    z_out[i] = zr;
+    nz = fma(zr, zr, nz);
+  }
+  return nz;
+}
+
 // nspec vectors of T are formed speculatively (warp 0) while the last warp
 // runs side() — every lane of it calls side(): the truncations decide their
 // rank there with the warp-level RANK, off the critical path; the count
@@ -1075,11 +1173,31 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
     double nz = 0.0;
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) nz = fma(z[i], z[i], nz);
-    const double rn = (nz > 0.0) ? rsqrt_f64(nz) : 0.0;
     double* zc = S.Z + LD * tid;
+#ifndef QTT_ZLO
+#define QTT_ZLO 1e-200
+#endif
+    if (!(nz > QTT_ZLO && nz < 1.0 / QTT_ZLO)) {
+      // the division-free determinants left the safe range (long T with tiny
+      // entries): ratio form (rare; out of line)
+      nz = twisted_ratio<NMAX>(S, n, lam, jc, zc);
+#pragma unroll
+      for (int i = 0; i < NMAX; ++i) z[i] = (i < n) ? zc[i] : 0.0;
+#ifdef QTT_FALLBACK_TRACE
+      printf("twisted ratio retry n=%d t=%d nz=%g\n", n, tid, nz);
+#endif
+    }
+    const double rn = (nz > 0.0) ? rsqrt_f64(nz) : 0.0;
 #pragma unroll
     for (int i = 0; i < NMAX; ++i) if (i < n) zc[i] = z[i] * rn;
-    if (!(nz > 0.0)) S.bad = 1;
+    if (!(nz > 0.0) || !(nz < 1e300)) {
+      // the division-free determinants under- or overflowed (long T with
+      // tiny entries): this vector comes from inverse iteration instead
+      atomicOr(&S.zbad, 1u << tid);
+#ifdef QTT_FALLBACK_TRACE
+      printf("twisted zero vector n=%d t=%d lam=%g r=%d\n", n, tid, lam, r);
+#endif
+    }
   }
   __syncthreads();
   const int nvec = nvec_smem ? (*nvec_smem < nspec ? *nvec_smem : nspec) : nspec;
@@ -1088,6 +1206,22 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
   //      modified Gram-Schmidt by warp 0, lane = component (n <= 32)
   if (tid < 32) {
     const int i = tid;
+    // vectors the twisted factorisation could not form, in ascending order
+    // (each orthogonal to the ones before it)
+    for (unsigned zb = S.zbad & ((nvec >= 32) ? 0xffffffffu : ((1u << nvec) - 1u)); zb; zb &= zb - 1u) {
+      const int a = __ffs(zb) - 1;
+      const double za = inverse_iter_vec<NMAX>(S, n, a, i);
+      const double nz = warp_sum(za * za);
+#ifdef QTT_FALLBACK_TRACE
+      if (i == 0) printf("zero vector a=%d n=%d -> inverse iteration %s\n", a, n, nz > 1e-6 ? "ok" : "FAILED");
+#endif
+      if (!(nz > 1e-6)) {
+        if (i == 0) S.bad = 1;
+      } else if (i < n) {
+        S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
+      }
+      __syncwarp();
+    }
     // no two kept eigenvalues within 1e-4: nothing to re-orthogonalise
     const bool near = i + 1 < nvec && S.lam[n - 1 - i] - S.lam[n - 2 - i] <= 1e-4;
     int c0 = __ballot_sync(0xffffffffu, near) ? 0 : nvec;
@@ -1101,9 +1235,23 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
           const double d = warp_sum(zb * za);
           za -= d * zb;
         }
-        const double nz = warp_sum(za * za);
+        double nz = warp_sum(za * za);
         if (!(nz > 1e-6)) {
-          if (i == 0) S.bad = 1;
+          // numerically dependent: inverse iteration with the shift lam_a
+          // from a fixed start vector, re-orthogonalised against every vector
+          // kept so far (the cluster's invariant subspace is what the
+          // truncation needs); the Jacobi fallback only if that fails too
+          za = inverse_iter_vec<NMAX>(S, n, a, i);
+          nz = warp_sum(za * za);
+#ifdef QTT_FALLBACK_TRACE
+          if (i == 0) printf("mgs dependent n=%d a=%d c0=%d c1=%d -> inverse iteration %s\n", n, a, c0, c1,
+                             nz > 1e-6 ? "ok" : "FAILED");
+#endif
+          if (!(nz > 1e-6)) {
+            if (i == 0) S.bad = 1;
+          } else if (i < n) {
+            S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
+          }
         } else if (i < n) {
           S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
         }
