@@ -60,7 +60,16 @@ __global__ void k_expand_prep(const ExProb* probs, ExParams P) {
   const ExProb& pr = probs[blockIdx.x];
   extern __shared__ __align__(16) unsigned char smraw[];
   cplx (*A)[256 * RC] = reinterpret_cast<cplx (*)[256 * RC]>(smraw);
+  // cores 2..ME staged in shared memory first (the products below would
+  // otherwise wait on a dependent chain of L2 loads per term)
+  cplx* cs = reinterpret_cast<cplx*>(smraw + 2 * 256 * RC * sizeof(cplx));
+  __shared__ int rk[ME + 1];
   const int tid = threadIdx.x;
+  if (tid <= ME) rk[tid] = pr.ranks[tid];
+  for (int e = tid; e < (ME - 1) * 2 * RC * RC; e += blockDim.x) {
+    const int m = e / (2 * RC * RC), o = e % (2 * RC * RC);
+    cs[e] = pr.cores[(size_t)(m + 1) * SLOT + o];   // core m + 2
+  }
   int r = pr.ranks[1];
   for (int e = tid; e < 2 * r; e += blockDim.x) {
     int i = e & 1, j = e >> 1;
@@ -69,8 +78,8 @@ __global__ void k_expand_prep(const ExProb* probs, ExParams P) {
   __syncthreads();
   int cur = 0;
   for (int k = 2; k <= ME; ++k) {
-    const cplx* c = pr.cores + (size_t)(k - 1) * SLOT;
-    const int r0 = r, r1 = pr.ranks[k];
+    const cplx* c = cs + (size_t)(k - 2) * 2 * RC * RC;
+    const int r0 = r, r1 = rk[k];
     const int h = 1 << (k - 1), n2 = 1 << k;
     for (int e = tid; e < n2 * r1; e += blockDim.x) {
       int i = e % n2, j = e / n2;
@@ -426,7 +435,7 @@ cudaError_t launch_fold_tail(const FoldProb* probs_dev, int nprob, int d, int l,
   return cudaGetLastError();
 }
 
-static constexpr size_t PREP_SMEM = 2 * 256 * RC * sizeof(cplx);
+static constexpr size_t PREP_SMEM = 2 * 256 * RC * sizeof(cplx) + (ME - 1) * 2 * RC * RC * sizeof(cplx);
 
 cudaError_t setup_expand_kernels() {
   cudaError_t e = cudaFuncSetAttribute(k_expand_main<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
