@@ -69,6 +69,7 @@ struct qtt_comm_s {
   int nshards;     // P (total shards)
   int nlocal;      // shards held by this process
   ncclComm_t nc;
+  ncclComm_t nc2;  // second communicator (ncclCommSplit of nc) for the g chain; null: one chain
 };
 
 struct qtt_tt_s {
@@ -523,6 +524,7 @@ struct NcclApi {
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
   const char* (*errStr)(ncclResult_t) = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;   // optional (NCCL >= 2.18)
 };
 
 // The NCCL already loaded in the process (PyTorch's) is preferred; else the
@@ -545,6 +547,7 @@ NcclApi& nccl_api() {
     a.groupStart = (decltype(a.groupStart))sym("ncclGroupStart");
     a.groupEnd = (decltype(a.groupEnd))sym("ncclGroupEnd");
     a.errStr = (decltype(a.errStr))sym("ncclGetErrorString");
+    a.commSplit = (decltype(a.commSplit))dlsym(h, "ncclCommSplit");
     a.ok = ok;
     if (!ok) a.err = "libnccl is missing a required symbol";
   });
@@ -659,11 +662,11 @@ void plan_sharded_dec(Carver& cv, const qtt_shape* s, const ShardGeom& g, int P,
 
 // Gram of the current level: per-CTA partials -> gsum (sum over the local
 // shards) -> sum over ranks (NCCL allreduce, f and g in one call).
-qtt_status reduce_grams(ShardDec& D, const qtt_comm_s* comm, int nblk, cudaStream_t st) {
+qtt_status reduce_grams(ShardDec& D, const qtt_comm_s* comm, ncclComm_t nc, int nblk, cudaStream_t st) {
   qtt_status r;
   if ((r = cuda_check(launch_gram_reduce(D.sh_dev, D.ntens, D.nlocal, nblk, st), "gram reduce"))) return r;
   if (comm->kind == 0)
-    return nccl_check(nccl_api().allReduce(D.gsum, D.gsum, (size_t)D.ntens * 1024, ncclDouble, ncclSum, comm->nc, st),
+    return nccl_check(nccl_api().allReduce(D.gsum, D.gsum, (size_t)D.ntens * 1024, ncclDouble, ncclSum, nc, st),
                       "ncclAllReduce(Gram)");
   return QTT_OK;
 }
@@ -671,7 +674,9 @@ qtt_status reduce_grams(ShardDec& D, const qtt_comm_s* comm, int nblk, cudaStrea
 // Alg. 1 over column shards: steps k <= d - l use the summed Grams; W is
 // gathered once the local unfolding is too narrow; the remaining steps run
 // redundantly on every rank on the (small) gathered W.
-qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, cudaStream_t st) {
+qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, cudaStream_t st,
+                           ncclComm_t nc_override = nullptr) {
+  ncclComm_t nc = nc_override ? nc_override : comm->nc;
   qtt_status r;
   if ((r = cuda_check(cudaMemcpyAsync(D.sh_dev, D.sh.data(), D.sh.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
                       "copy descriptors")))
@@ -682,19 +687,19 @@ qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, c
   const int d = D.d, dl = D.dl, nsh = (int)D.sh.size();
   int nblk = dec_nblk_loc(dl, nsh);
   if ((r = cuda_check(launch_level_gram(D.sh_dev, nsh, nblk, prm.status, st), "level gram"))) return r;
-  if ((r = reduce_grams(D, comm, nblk, st))) return r;
+  if ((r = reduce_grams(D, comm, nc, nblk, st))) return r;
   if ((r = cuda_check(launch_level_solve(D.tn_dev, D.ntens, 0, prm, st), "level solve"))) return r;
   int k = 5;
   nblk = proj_nblk(1 << (dl - k), nsh);
   if ((r = cuda_check(launch_project(true, D.sh_dev, nsh, k, nblk, 1, st), "project"))) return r;
-  if ((r = reduce_grams(D, comm, nblk, st))) return r;
+  if ((r = reduce_grams(D, comm, nc, nblk, st))) return r;
   int src_is_a = 1;
   ++k;
   while ((1ll << (dl - k + 1)) >= 256 && (1ll << (d - k + 1)) > FIN_COLS_HOST) {
     if ((r = cuda_check(launch_step_solve(D.tn_dev, D.ntens, k, 0, prm, st), "step solve"))) return r;
     nblk = proj_nblk(1 << (dl - k), nsh);
     if ((r = cuda_check(launch_project(false, D.sh_dev, nsh, k, nblk, src_is_a, st), "project"))) return r;
-    if ((r = reduce_grams(D, comm, nblk, st))) return r;
+    if ((r = reduce_grams(D, comm, nc, nblk, st))) return r;
     src_is_a ^= 1;
     ++k;
   }
@@ -706,7 +711,7 @@ qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, c
     for (int t = 0; t < D.ntens; ++t) {
       const double* src = src_is_a ? D.sh[t].Wa : D.sh[t].Wb;
       double* dst = D.gath + (size_t)t * D.P * RS_GATHER * nl;
-      if ((r = nccl_check(A.allGather(src, dst, (size_t)RS_GATHER * nl, ncclDouble, comm->nc, st), "ncclAllGather(W)"))) {
+      if ((r = nccl_check(A.allGather(src, dst, (size_t)RS_GATHER * nl, ncclDouble, nc, st), "ncclAllGather(W)"))) {
         A.groupEnd();
         return r;
       }
@@ -795,8 +800,17 @@ size_t ws_sharded(const qtt_shape* shape, const qtt_trunc* fft, int P, int nloca
   TTAlloc tt[2] = {take_tt(cv, 1, d), take_tt(cv, 1, d)};
   TTAlloc Y = take_tt(cv, 1, d);
   const double* xs[2] = {nullptr, nullptr};
+  // the two-chain plan (two single-tensor plans) needs at least as much as
+  // the batched one; size for both
+  const size_t off0 = cv.off;
   ShardDec D;
   plan_sharded_dec(cv, shape, g, P, nlocal, 0, 2, xs, tt, D);
+  const size_t one = cv.off;
+  cv.off = off0;
+  ShardDec Df, Dg;
+  plan_sharded_dec(cv, shape, g, P, nlocal, 0, 1, xs, tt, Df);
+  plan_sharded_dec(cv, shape, g, P, nlocal, 0, 1, xs + 1, tt + 1, Dg);
+  if (cv.off < one) cv.off = one;
   run_convolve(tt[0].cores, tt[0].ranks, 1, tt[1].cores, tt[1].ranks, 1, shape, fft, nullptr, 1.0, Y, cv, nullptr,
                nullptr, RS_GATHER);
   ShardEx E;
@@ -1063,12 +1077,35 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
   prof_mark(0, st);
   DecParams prm = dec_params(dec, status);
   if (comm) {
-    // Step 1-2 column-sharded: f and g shards in one sequence, one allreduce per level
+    // Step 1-2 column-sharded.  With a second communicator (or a virtual one)
+    // f and g run as two chains on two streams, as on one GPU: the one-CTA
+    // solves and the allreduces of one hide under the passes of the other;
+    // each chain issues its collectives on its own communicator, so the two
+    // streams never interleave operations of one NCCL communicator.
+    // Otherwise: one batched chain, one allreduce per level for f and g.
     const double* xs[2] = {f, g};
     TTAlloc tts[2] = {F, G};
-    ShardDec D;
-    plan_sharded_dec(cv, shape, geo, comm->nshards, comm->nlocal, comm_first(comm), 2, xs, tts, D);
-    if ((r = run_sharded_dec(D, comm, prm, st))) return r;
+    cudaStream_t side = (comm->kind == 1 || comm->nc2) && g_prof < 2 ? side_stream() : nullptr;
+    if (side) {
+      ShardDec Df, Dg;
+      plan_sharded_dec(cv, shape, geo, comm->nshards, comm->nlocal, comm_first(comm), 1, xs, tts, Df);
+      plan_sharded_dec(cv, shape, geo, comm->nshards, comm->nlocal, comm_first(comm), 1, xs + 1, tts + 1, Dg);
+      cudaEvent_t fork = nullptr, join = nullptr;
+      if ((r = cuda_check(evg.make(&fork, cudaEventDisableTiming), "event"))) return r;
+      if ((r = cuda_check(evg.make(&join, cudaEventDisableTiming), "event"))) return r;
+      cudaEventRecord(fork, st);
+      cudaStreamWaitEvent(side, fork, 0);
+      r = run_sharded_dec(Dg, comm, prm, side, comm->nc2);
+      if (!r) r = run_sharded_dec(Df, comm, prm, st);
+      // the join is recorded even after a failed launch (see the one-GPU path)
+      cudaEventRecord(join, side);
+      qtt_status rj = cuda_check(cudaStreamWaitEvent(st, join, 0), "join");
+      if (r || (r = rj)) return r;
+    } else {
+      ShardDec D;
+      plan_sharded_dec(cv, shape, geo, comm->nshards, comm->nlocal, comm_first(comm), 2, xs, tts, D);
+      if ((r = run_sharded_dec(D, comm, prm, st))) return r;
+    }
   } else {
     // Step 1-2: all signals and the kernel(s) in one batched TT-SVD
     const int d_ = d;
@@ -1267,8 +1304,13 @@ qtt_status qtt_comm_init(const unsigned char id_host[128], int nranks, int rank,
   ncclComm_t nc;
   qtt_status r;
   if ((r = nccl_check(A.commInitRank(&nc, nranks, id, rank), "ncclCommInitRank"))) return r;
-  qtt_comm_t c = new (std::nothrow) qtt_comm_s{0, nranks, rank, nranks, 1, nc};
+  // a second communicator over the same ranks for the g chain of the
+  // sharded TT-SVD (collective; without ncclCommSplit the chains are batched)
+  ncclComm_t nc2 = nullptr;
+  if (A.commSplit && A.commSplit(nc, 0, rank, &nc2, nullptr) != ncclSuccess) nc2 = nullptr;
+  qtt_comm_t c = new (std::nothrow) qtt_comm_s{0, nranks, rank, nranks, 1, nc, nc2};
   if (!c) {
+    if (nc2) A.commDestroy(nc2);
     A.commDestroy(nc);
     return fail(QTT_ENOMEM, "host allocation failed");
   }
@@ -1288,6 +1330,7 @@ qtt_status qtt_comm_init_virtual(int nshards, qtt_comm_t* out) {
 
 void qtt_comm_destroy(qtt_comm_t c) {
   if (!c) return;
+  if (c->kind == 0 && c->nc2) nccl_api().commDestroy(c->nc2);
   if (c->kind == 0 && c->nc) nccl_api().commDestroy(c->nc);
   delete c;
 }
