@@ -1088,6 +1088,45 @@ __device__ __noinline__ double twisted_ratio(TridSmem<NMAX>& S, int n, double la
   return nz;
 }
 
+// Out-of-line repair of the vectors in `bad` (bit a = vector a): each one,
+// in ascending order, from inverse iteration (inverse_iter_vec: orthogonal to
+// every vector before it), then one modified Gram-Schmidt pass over all nvec
+// vectors so the whole set is orthonormal again.  A vector that stays
+// dependent sets S.bad (the caller falls back to Jacobi).  Warp 0, lane i =
+// component.
+template <int NMAX>
+__device__ __noinline__ void repair_vectors(TridSmem<NMAX>& S, int n, int nvec, unsigned bad, int i) {
+  constexpr int LD = NMAX + 1;
+  for (unsigned zb = bad; zb; zb &= zb - 1u) {
+    const int a = __ffs(zb) - 1;
+    const double za = inverse_iter_vec<NMAX>(S, n, a, i);
+    const double nz = warp_sum(za * za);
+#ifdef QTT_FALLBACK_TRACE
+    if (i == 0) printf("repair vector a=%d n=%d -> inverse iteration %s\n", a, n, nz > 1e-6 ? "ok" : "FAILED");
+#endif
+    if (!(nz > 1e-6)) {
+      if (i == 0) S.bad = 1;
+    } else if (i < n) {
+      S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
+    }
+    __syncwarp();
+  }
+  for (int a = 1; a < nvec; ++a) {
+    double za = (i < n) ? S.Z[LD * a + i] : 0.0;
+    for (int b = 0; b < a; ++b) {
+      const double zb = (i < n) ? S.Z[LD * b + i] : 0.0;
+      za -= warp_sum(zb * za) * zb;
+    }
+    const double nz = warp_sum(za * za);
+    if (!(nz > 1e-6)) {
+      if (i == 0) S.bad = 1;
+    } else if (i < n) {
+      S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
+    }
+    __syncwarp();
+  }
+}
+
 // nspec vectors of T are formed speculatively (warp 0) while the last warp
 // runs side() — every lane of it calls side(): the truncations decide their
 // rank there with the warp-level RANK, off the critical path; the count
@@ -1206,25 +1245,10 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
   //      modified Gram-Schmidt by warp 0, lane = component (n <= 32)
   if (tid < 32) {
     const int i = tid;
-    // vectors the twisted factorisation could not form, in ascending order
-    // (each orthogonal to the ones before it)
-    for (unsigned zb = S.zbad & ((nvec >= 32) ? 0xffffffffu : ((1u << nvec) - 1u)); zb; zb &= zb - 1u) {
-      const int a = __ffs(zb) - 1;
-      const double za = inverse_iter_vec<NMAX>(S, n, a, i);
-      const double nz = warp_sum(za * za);
-#ifdef QTT_FALLBACK_TRACE
-      if (i == 0) printf("zero vector a=%d n=%d -> inverse iteration %s\n", a, n, nz > 1e-6 ? "ok" : "FAILED");
-#endif
-      if (!(nz > 1e-6)) {
-        if (i == 0) S.bad = 1;
-      } else if (i < n) {
-        S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
-      }
-      __syncwarp();
-    }
     // no two kept eigenvalues within 1e-4: nothing to re-orthogonalise
     const bool near = i + 1 < nvec && S.lam[n - 1 - i] - S.lam[n - 2 - i] <= 1e-4;
     int c0 = __ballot_sync(0xffffffffu, near) ? 0 : nvec;
+    unsigned dep = 0u;   // vectors found numerically dependent (left for repair)
     while (c0 < nvec) {
       int c1 = c0 + 1;
       while (c1 < nvec && S.lam[n - 1 - (c1 - 1)] - S.lam[n - 1 - c1] <= 1e-4) ++c1;
@@ -1235,30 +1259,17 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
           const double d = warp_sum(zb * za);
           za -= d * zb;
         }
-        double nz = warp_sum(za * za);
-        if (!(nz > 1e-6)) {
-          // numerically dependent: inverse iteration with the shift lam_a
-          // from a fixed start vector, re-orthogonalised against every vector
-          // kept so far (the cluster's invariant subspace is what the
-          // truncation needs); the Jacobi fallback only if that fails too
-          za = inverse_iter_vec<NMAX>(S, n, a, i);
-          nz = warp_sum(za * za);
-#ifdef QTT_FALLBACK_TRACE
-          if (i == 0) printf("mgs dependent n=%d a=%d c0=%d c1=%d -> inverse iteration %s\n", n, a, c0, c1,
-                             nz > 1e-6 ? "ok" : "FAILED");
-#endif
-          if (!(nz > 1e-6)) {
-            if (i == 0) S.bad = 1;
-          } else if (i < n) {
-            S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
-          }
-        } else if (i < n) {
-          S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
-        }
+        const double nz = warp_sum(za * za);
+        if (!(nz > 1e-6)) dep |= 1u << a;
+        else if (i < n) S.Z[LD * a + i] = za * (1.0 / sqrt(nz));
         __syncwarp();
       }
       c0 = c1;
     }
+    // rare: vectors the twisted factorisation could not form (zbad) or that
+    // came out dependent inside a cluster — rebuilt out of line
+    const unsigned mask = (nvec >= 32) ? 0xffffffffu : ((1u << nvec) - 1u);
+    if ((S.zbad & mask) | dep) repair_vectors<NMAX>(S, n, nvec, (S.zbad & mask) | dep, i);
   }
   __syncthreads();
   if (tid == 0) { long long t = clock64(); S.tph[3] = t - tt0; tt0 = t; }
