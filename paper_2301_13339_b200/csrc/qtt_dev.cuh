@@ -1408,7 +1408,7 @@ __device__ __forceinline__ void small_mm(cplx* C, const cplx* X, const cplx* Y, 
 }
 
 template <int NMAX, int NT>
-__device__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
+__device__ __noinline__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* status) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x;
   const int N = n + (n & 1);
@@ -1844,7 +1844,7 @@ __device__ __forceinline__ void omega_pair(unsigned long long j, unsigned k, uns
 // SV drop-off rule (modification (3); oracle rank_rule_dropoff):
 // first k with lam_{k+1} < delta^2 lam_k, no drop: lam_k >= 1e-14 lam_1;
 // then the cap, moved down out of a cluster when it binds.
-__device__ __forceinline__ int rank_rule_dropoff(const double* lam, int m, double delta, int rmax, double ctol) {
+static __device__ __noinline__ int rank_rule_dropoff(const double* lam, int m, double delta, int rmax, double ctol) {
   if (m <= 0) return 1;
   const double l0 = fmax(lam[0], 0.0);
   if (!(l0 > 0.0)) return 1;
