@@ -375,9 +375,11 @@ __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const doubl
 #else
 #define TRID_KLOOP _Pragma("unroll")
 #endif
-template <int NMAX, int NT>
-__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm,
-                            bool real_in = false) {
+// REAL: the matrix is real symmetric (TT-SVD Grams) — the real one-warp path
+// for NMAX <= 20; a compile-time choice, so a complex solver carries none of
+// the real path's code and vice versa
+template <int NMAX, int NT, bool REAL = false>
+__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x, lane = tid & 31;
   double anrm = 0.0;
@@ -607,10 +609,9 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       }
     }
   } else {
-  bool done = false;
-  if constexpr (NMAX <= 20) {
-    if (real_in) {
-      done = true;
+  constexpr bool done = REAL && NMAX <= 20;
+  if constexpr (NMAX <= 20 && REAL) {
+    {
       // ---- real symmetric A, n <= 20 (every TT-SVD step Gram at R_max <= 10:
       //      the unfoldings are real): ONE warp, lane i = row i with all
       //      NMAX columns of the (normalised, zero-padded) matrix in
@@ -745,7 +746,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       }
     }
   }
-  if (!done) {
+  if constexpr (!done) {
   if (wp < 4) {
     // Warps 0-3 (one per SM sub-partition, so the FP64 pipes of all four
     // are used): lane i = row i, warp w owns columns j = w + 4t of the
@@ -1644,8 +1645,8 @@ __device__ __noinline__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* sta
 //                                eigenvalues (column-major, ld NMAX+1).
 // Tridiagonal solver first; Jacobi (whole problem again) if it reports a
 // dependent cluster (status bit ST_FALLBACK).
-template <int NMAX, int NT>
-__device__ void eig_values(EigSmem<NMAX>& E, int n, bool real_in = false) {
+template <int NMAX, int NT, bool REAL = false>
+__device__ void eig_values(EigSmem<NMAX>& E, int n) {
   constexpr int LD = NMAX + 1;
   if constexpr (NMAX <= 16) {
     // single-warp path: E.A[0] is read, not modified (padding handled in
@@ -1659,7 +1660,7 @@ __device__ void eig_values(EigSmem<NMAX>& E, int n, bool real_in = false) {
     else E.A[0][i + LD * j] = czero();   // the tridiagonalisation runs on the zero-padded matrix
   }
   __syncthreads();
-  trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1], real_in);
+  trid_values<NMAX, NT, REAL>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1]);
 }
 
 #ifdef QTT_EIG_CHECK

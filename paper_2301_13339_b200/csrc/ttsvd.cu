@@ -452,7 +452,7 @@ __device__ int rsvd_truncate(EigSmem<NE>& E, RsvdBuf& R, int rr, int kp, double 
     E.A[0][i + LD * j] = cmk(t, 0.0);
   }
   __syncthreads();
-  eig_values<NE, NT>(E, rr, true);
+  eig_values<NE, NT, true>(E, rr);
   const cplx* Q = eig_vectors<NE, NT>(E, rr, kp, prm.status);
   for (int e = tid; e < rr * kp; e += NT) {
     const int i = e % rr, c = e / rr;
@@ -474,7 +474,7 @@ __device__ int rsvd_truncate(EigSmem<NE>& E, RsvdBuf& R, int rr, int kp, double 
     E.A[0][a + LD * b] = cmk(t, 0.0);
   }
   __syncthreads();
-  eig_values<NE, NT>(E, kp, true);
+  eig_values<NE, NT, true>(E, kp);
   if (tid == 0) R.rk = rank_choose(E.lam, kp, tau2, prm.rmax, prm.ctol, 0, 0.0);
   __syncthreads();
   const int rk = R.rk;
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(NT, 1) k_level_solve(const DecProb* probs, int
       rk = rsvd_truncate<NE>(S.E, S.R, rr, prm.kp, tau2, prm);
       write_core_from_Ud(pr, k, S.R.UB, rr, rk);
     } else {
-      eig_values<NE, NT>(S.E, rr, true);
+      eig_values<NE, NT, true>(S.E, rr);
       if (tid == 0) {
         int mp = rr < (1 << (d - k)) ? rr : (1 << (d - k));
         S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta, prm.status);
@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_solve(const DecProb* probs, int 
 #ifdef QTT_STEP_TIMING
   long long c0 = clock64();
 #endif
-  eig_values<NE, NT>(S.E, rr, true);
+  eig_values<NE, NT, true>(S.E, rr);
 #ifdef QTT_STEP_TIMING
   long long c1 = clock64();
 #endif
@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(NT, 1) k_finish(const DecProb* probs, int ksta
       rk = rsvd_truncate<NE>(S.E, S.R, rr, prm.kp, tau2, prm);
       write_core_from_Ud(pr, k, S.R.UB, rr, rk);
     } else {
-      eig_values<NE, NT>(S.E, rr, true);
+      eig_values<NE, NT, true>(S.E, rr);
       if (tid == 0) {
         int mp = rr < n ? rr : n;
         S.rk = rank_choose(S.E.lam, mp, tau2, prm.rmax, prm.ctol, prm.rule, prm.delta, prm.status);
