@@ -173,6 +173,32 @@ struct EventGuard {
 // The TT-SVD chunk loaders read the inputs with 16-byte cp.async copies
 // (ttsvd.cu load_chunk_async): every array (and every batch entry) must
 // start on a 16-byte boundary.
+// Descriptor upload without the copy engine: the (small) host descriptor
+// arrays go to device memory through a kernel whose parameter carries the
+// bytes.  A cudaMemcpyAsync here would queue behind whatever the copy engine
+// is moving for the caller (e.g. the next step's inputs on a copy stream) and
+// stall the compute stream; it would also be a pageable copy, which cannot be
+// captured in a CUDA graph.
+struct DescChunk {
+  unsigned int n;
+  unsigned char b[2044];
+};
+__global__ void k_store_desc(unsigned char* dst, const DescChunk c) {
+  for (unsigned int i = threadIdx.x; i < c.n; i += blockDim.x) dst[i] = c.b[i];
+}
+cudaError_t upload_desc(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  const unsigned char* sp = static_cast<const unsigned char*>(src);
+  unsigned char* dp = static_cast<unsigned char*>(dst);
+  for (size_t off = 0; off < bytes; off += sizeof(DescChunk::b)) {
+    DescChunk c;
+    c.n = (unsigned int)((bytes - off) < sizeof(c.b) ? (bytes - off) : sizeof(c.b));
+    memcpy(c.b, sp + off, c.n);
+    k_store_desc<<<1, 128, 0, st>>>(dp + off, c);
+    count_launches(1);
+  }
+  return cudaGetLastError();
+}
+
 qtt_status check_input_align(const double* x, long long stride, int n, const char* which) {
   if (((uintptr_t)x & 15) != 0) return fail(QTT_EINVAL, "%s must be 16-byte aligned", which);
   if (n > 1 && (stride & 1)) return fail(QTT_EINVAL, "%s batch stride must be even (16-byte aligned entries)", which);
@@ -330,7 +356,7 @@ qtt_status run_decompose(const double* base, long long stride, int n, const qtt_
   DecProb* dp = cv.take<DecProb>(n);
   if (!cv.base) return QTT_OK;
   qtt_status r;
-  if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), n * sizeof(DecProb), cudaMemcpyHostToDevice, st),
+  if ((r = cuda_check(upload_desc(dp, h.data(), n * sizeof(DecProb), st),
                       "copy descriptors")))
     return r;
   DecParams prm = dec_params(dec, status);
@@ -360,7 +386,7 @@ qtt_status run_transform(const std::vector<XfProb>& hv, const qtt_shape* s, cons
   P.shift[1] = (shift && s->D == 2) ? shift[1] : 0;
   P.status = status;
   qtt_status r;
-  if ((r = cuda_check(cudaMemcpyAsync(dp, hv.data(), n * sizeof(XfProb), cudaMemcpyHostToDevice, st),
+  if ((r = cuda_check(upload_desc(dp, hv.data(), n * sizeof(XfProb), st),
                       "copy descriptors")))
     return r;
   return cuda_check(launch_transform(dp, n, P, st), "transform launch");
@@ -379,7 +405,7 @@ qtt_status run_expand(const cplx* cores, const int* ranks, int nt, int d, double
   if (!cv.base) return QTT_OK;
   ExParams P{d, s->layout, s->bits[0], imag, rcap};
   qtt_status r;
-  if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), nt * sizeof(ExProb), cudaMemcpyHostToDevice, st),
+  if ((r = cuda_check(upload_desc(dp, h.data(), nt * sizeof(ExProb), st),
                       "copy descriptors")))
     return r;
   return cuda_check(launch_expand(dp, nt, P, st), "expand launch");
@@ -488,16 +514,16 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
   if (cv.base) {
     HrParams H{d, fft->eps, fft->rmax, fft->cluster_tol, status, fft->rule, fft->delta, gr_multi ? 1 : 0};
     if (big) {
-      if ((r = cuda_check(cudaMemcpyAsync(hbp, hb.data(), nf * sizeof(HrBigProb), cudaMemcpyHostToDevice, st),
+      if ((r = cuda_check(upload_desc(hbp, hb.data(), nf * sizeof(HrBigProb), st),
                           "copy descriptors")))
         return r;
       if ((r = cuda_check(launch_hadamard_round_big(hbp, nf, H, st), "hadamard/round launch"))) return r;
     } else {
-      if ((r = cuda_check(cudaMemcpyAsync(hp, hr.data(), nf * sizeof(HrProb), cudaMemcpyHostToDevice, st),
+      if ((r = cuda_check(upload_desc(hp, hr.data(), nf * sizeof(HrProb), st),
                           "copy descriptors")))
         return r;
       if (gr_multi) {
-        if ((r = cuda_check(cudaMemcpyAsync(hbp, hb.data(), nf * sizeof(HrBigProb), cudaMemcpyHostToDevice, st),
+        if ((r = cuda_check(upload_desc(hbp, hb.data(), nf * sizeof(HrBigProb), st),
                             "copy descriptors")))
           return r;
         if ((r = cuda_check(launch_hr_gr_chain(hbp, nf, d, st), "right-Gram chain launch"))) return r;
@@ -678,10 +704,10 @@ qtt_status run_sharded_dec(ShardDec& D, const qtt_comm_s* comm, DecParams prm, c
                            ncclComm_t nc_override = nullptr) {
   ncclComm_t nc = nc_override ? nc_override : comm->nc;
   qtt_status r;
-  if ((r = cuda_check(cudaMemcpyAsync(D.sh_dev, D.sh.data(), D.sh.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
+  if ((r = cuda_check(upload_desc(D.sh_dev, D.sh.data(), D.sh.size() * sizeof(DecProb), st),
                       "copy descriptors")))
     return r;
-  if ((r = cuda_check(cudaMemcpyAsync(D.tn_dev, D.tn.data(), D.tn.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
+  if ((r = cuda_check(upload_desc(D.tn_dev, D.tn.data(), D.tn.size() * sizeof(DecProb), st),
                       "copy descriptors")))
     return r;
   const int d = D.d, dl = D.dl, nsh = (int)D.sh.size();
@@ -772,10 +798,10 @@ qtt_status run_sharded_expand(ShardEx& E, const qtt_shape* s, const ShardGeom& g
                               int rcap = RC) {
   qtt_status r;
   const int n = (int)E.fp.size();
-  if ((r = cuda_check(cudaMemcpyAsync(E.fp_dev, E.fp.data(), n * sizeof(FoldProb), cudaMemcpyHostToDevice, st),
+  if ((r = cuda_check(upload_desc(E.fp_dev, E.fp.data(), n * sizeof(FoldProb), st),
                       "copy descriptors")))
     return r;
-  if ((r = cuda_check(cudaMemcpyAsync(E.ex_dev, E.ex.data(), n * sizeof(ExProb), cudaMemcpyHostToDevice, st),
+  if ((r = cuda_check(upload_desc(E.ex_dev, E.ex.data(), n * sizeof(ExProb), st),
                       "copy descriptors")))
     return r;
   if ((r = cuda_check(launch_fold_tail(E.fp_dev, n, d, g.l, st), "fold tail"))) return r;
@@ -1128,7 +1154,7 @@ qtt_status qtt_conv_full(const double* f, const double* g, double* y, const qtt_
       p.seed = dec->seed + (unsigned long long)i;   // f batch entries, then g
     }
     DecProb* dp = cv.take<DecProb>(nf + ng);
-    if ((r = cuda_check(cudaMemcpyAsync(dp, h.data(), h.size() * sizeof(DecProb), cudaMemcpyHostToDevice, st),
+    if ((r = cuda_check(upload_desc(dp, h.data(), h.size() * sizeof(DecProb), st),
                         "copy descriptors")))
       return r;
     const int ntot = nf + ng;
