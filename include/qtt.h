@@ -21,8 +21,14 @@
  *     the decomposition of g onto a library-owned non-blocking stream of the
  *     current device and joins it back with events before Step 3, so all
  *     of its work stays ordered after earlier and before later work on
- *     `stream`.  Calls copy small descriptor arrays from host memory
- *     (cudaMemcpyAsync); they are not meant for CUDA graph capture.
+ *     `stream`.  The small per-call descriptor arrays reach the device
+ *     through a kernel's parameters (no copy-engine or pageable copy on
+ *     `stream`), so qtt_conv_full / qtt_decompose / qtt_convolve /
+ *     qtt_to_full without a report can be captured in a CUDA graph on
+ *     `stream` (the side-stream fork / join is captured with it; replays
+ *     reuse the descriptors and workspace layout of the captured call, so the
+ *     shape, policy, pointers and workspace must not change between
+ *     replays).  Calls with `rep_host` synchronise and cannot be captured.
  *   - No call allocates device memory: all scratch and all device storage of
  *     TT handles is carved from the caller's workspace `ws` (>= the size
  *     returned by qtt_workspace_bytes, 256-byte aligned).  The workspace must
