@@ -174,18 +174,42 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     for (int e = tid; e < rz * rz; e += NT) S.Y[e] = pr.gr[(size_t)c * GR_HR + e];
     __syncthreads();
     HT_MARK(0)
-    for (int e = tid; e < rows * rz; e += NT) {
-      int i = e % rows, j = e / rows;
-      cplx s = czero();
-      for (int l = 0; l < rz; ++l) s = cfma(S.Eb[i + rows * l], S.Y[l + rz * j], s);
-      S.Y2[e] = s;
-    }
+    // T = E GR (rows x rz, k = rz <= 64) and K = T E^H (rows x rows, k = rz)
+    // on DMMA tiles (16 warps: one 8 x 8 tile of T each; the 4 tiles of K
+    // with their k-chunks split over the warps and summed in a fixed order)
+    cgemm_dmma<NT / 32>(
+        rows, rz, rz,
+        [&](int i, int l) { return (i < rows && l < rz) ? S.Eb[i + rows * l] : czero(); },
+        [&](int l, int j) { return (l < rz && j < rz) ? S.Y[l + rz * j] : czero(); },
+        [&](int i, int j, cplx v) { if (i < rows && j < rz) S.Y2[i + rows * j] = v; });
     __syncthreads();
-    for (int e = tid; e < rows * rows; e += NT) {
-      int i = e % rows, j = e / rows;
-      cplx s = czero();
-      for (int l = 0; l < rz; ++l) s = cfma_bc(S.Y2[i + rows * l], S.Eb[j + rows * l], s);
-      S.E.A[0][i + LD * j] = s;
+    {
+      // K: tile t = w & 3 (2 x 2 tiles of 8 at rows <= 16), k-split ks = w >> 2
+      const int lane = tid & 31, wq = tid >> 5, t = wq & 3, ks = wq >> 2;
+      const int ar = lane >> 2, ac = lane & 3, ti = t & 1, tj = t >> 1;
+      double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
+      const int nk = (rz + 3) >> 2;
+      for (int kc = ks; kc < nk; kc += 4) {
+        const int k = 4 * kc + ac, ri = 8 * ti + ar, cj = 8 * tj + ar;
+        const cplx a = (ri < rows && k < rz) ? S.Y2[ri + rows * k] : czero();
+        const cplx b = (k < rz && cj < rows) ? cconj(S.Eb[cj + rows * k]) : czero();
+        dmma884(r0, r1, a.x, b.x);
+        dmma884(r0, r1, -a.y, b.y);
+        dmma884(i0, i1, a.x, b.y);
+        dmma884(i0, i1, a.y, b.x);
+      }
+      cplx* part = S.Y;    // 16 x 64 partial tiles (GR is consumed by T)
+      part[wq * 64 + ar * 8 + 2 * ac] = cmk(r0, i0);
+      part[wq * 64 + ar * 8 + 2 * ac + 1] = cmk(r1, i1);
+      __syncthreads();
+      if (tid < 256) {
+        const int tt = tid >> 6, pos = tid & 63;
+        const int i = 8 * (tt & 1) + (pos >> 3), j = 8 * (tt >> 1) + (pos & 7);
+        cplx v = part[tt * 64 + pos];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) v = cadd(v, part[(tt + 4 * q) * 64 + pos]);
+        if (i < rows && j < rows) S.E.A[0][i + LD * j] = v;
+      }
     }
     __syncthreads();
     if (c == 1) {
