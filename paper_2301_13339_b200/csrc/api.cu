@@ -526,7 +526,7 @@ qtt_status run_convolve(const cplx* fc, const int* fr, int nf, const cplx* gc, c
         if ((r = cuda_check(upload_desc(hbp, hb.data(), nf * sizeof(HrBigProb), st),
                             "copy descriptors")))
           return r;
-        if ((r = cuda_check(launch_hr_gr_chain(hbp, nf, d, st), "right-Gram chain launch"))) return r;
+        if ((r = cuda_check(launch_hr_gr_chain_cluster(hbp, nf, d, st), "right-Gram chain launch"))) return r;
       }
       if ((r = cuda_check(launch_hadamard_round(hp, nf, H, st), "hadamard/round launch"))) return r;
     }

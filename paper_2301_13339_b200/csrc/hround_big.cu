@@ -15,6 +15,8 @@
 //   sweep, per cut c (1 .. d-1):
 //     T = E GR_c, K = T E^H, eigenpairs, RANK, core c = U_r, Sm = U_r^H E,
 //     H = Sm x G_{c+1}, E <- H x F_{c+1}.
+#include <cooperative_groups.h>
+
 #include "qtt_kernels.h"
 
 namespace qtt {
@@ -237,9 +239,6 @@ __global__ void k_hrb_final(const HrBigProb* probs, int d) {
   for (int q = threadIdx.x; q <= d; q += NT) p.out_ranks[q] = (q == 0 || q == d) ? 1 : p.st[2 + q];
 }
 
-cudaError_t setup_hr_big_kernels() {
-  return cudaFuncSetAttribute(k_hrb_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HrbSolveSmem));
-}
 
 size_t hr_big_scratch(int d) {
   // gr (d slots) + t1/t2/t3 (2 slices each) + e, tb, sm, hb (complex) ; st, tau2 separate
@@ -258,6 +257,132 @@ static int launch_hr_gr_chain_impl(const HrBigProb* probs_dev, int nprob, int d,
     }
   }
   return n;
+}
+
+// ------------------------------------------- cluster form (ranks <= 8)
+// The right-Gram chain of Z = F (.) G for Rhat <= 8 (rz <= 64) in ONE launch:
+// a cluster of 8 CTAs per tensor, CTA r owning the column group with F index
+// r of every matrix (GR_c columns (r, k'), T1..T3 columns (r, e')), so the
+// three mode products A1, A2, B1 are CTA-local; B2 sums over the F index:
+// each CTA forms its partial P_r[:, (e, e')] = sum_al T3_al[:, (r, e')]
+// conj(F[e, al, r]) for all e, and CTA e adds the partials of every CTA
+// (distributed shared memory, ascending r: deterministic) for its column
+// group — exactly the layout the next core needs.  Two cluster barriers per
+// core instead of four grid-wide launches; every GR slot is also written to
+// global memory for the sweep (layout of launch_hr_gr_chain).
+static constexpr int CLR = 8;
+struct GrClSmem {
+  cplx grs[64 * 8];            // own column group of GR_c (rows rzx, ld 64)
+  cplx t1[2][64 * 8];          // per slice al: T1 / T3 (rows, ld 64)
+  cplx t2[2][64 * 8];          // T2
+  cplx part[64 * 64];          // P_r (rows rzo x fa ga columns, ld 64)
+  cplx fc[2 * 8 * 8], gc[2 * 8 * 8];
+  int rf[MAXD + 1], rg[MAXD + 1];
+};
+__global__ void __cluster_dims__(CLR, 1, 1) __launch_bounds__(NT) k_hr_gr_cluster(const HrBigProb* probs, int d) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const HrBigProb& p = probs[blockIdx.y];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  GrClSmem& S = *reinterpret_cast<GrClSmem*>(smraw);
+  const int r = (int)cl.block_rank(), tid = threadIdx.x;
+  for (int q = tid; q <= d; q += NT) { S.rf[q] = p.f_ranks[q]; S.rg[q] = p.g_ranks[q]; }
+  __syncthreads();
+  // GR_{d-1}[(a,a'),(b,b')] = sum_al Z[(a,a'),al] conj(Z[(b,b'),al]), Z = F_d[.,al] G_d[.,al]
+  {
+    const int af = S.rf[d - 1], ag = S.rg[d - 1], rz = af * ag;
+    const cplx* F = fcore(p, d);
+    const cplx* G = gcore(p, d);
+    cplx* slot = p.gr + (size_t)(d - 1) * GR_HR;
+    if (r < af)
+      for (int e = tid; e < rz * ag; e += NT) {
+        const int i = e % rz, jj = e / rz, ia = i / ag, ib = i % ag;
+        cplx s = czero();
+        for (int al = 0; al < 2; ++al) {
+          const cplx zi = cmul(F[ia + af * al], G[ib + ag * al]);
+          const cplx zj = cmul(F[r + af * al], G[jj + ag * al]);
+          s = cfma_bc(zi, zj, s);
+        }
+        S.grs[i + 64 * jj] = s;
+        slot[i + rz * (r * ag + jj)] = s;
+      }
+  }
+  for (int c = d - 1; c >= 2; --c) {
+    const int fa = S.rf[c - 1], fb = S.rf[c], ga = S.rg[c - 1], gb = S.rg[c];
+    const int rzx = fb * gb, ra = fb * ga, rzo = fa * ga;
+    {
+      const cplx* F = fcore(p, c);
+      const cplx* G = gcore(p, c);
+      for (int e = tid; e < 2 * fa * fb; e += NT) S.fc[e] = F[e];
+      for (int e = tid; e < 2 * ga * gb; e += NT) S.gc[e] = G[e];
+    }
+    __syncthreads();
+    const cplx* F = S.fc;
+    const cplx* G = S.gc;
+    if (r < fb) {
+      // A1: T1_al[(b,a'), jj] = sum_b' G[a',al,b'] GR_c[(b,b'), (r, jj)]
+      for (int e = tid; e < 2 * ra * gb; e += NT) {
+        const int al = e / (ra * gb), o = e % (ra * gb), i = o % ra, jj = o / ra;
+        const int b = i / ga, ap = i % ga;
+        cplx s = czero();
+        for (int bp = 0; bp < gb; ++bp) s = cfma(G[ap + ga * al + 2 * ga * bp], S.grs[(b * gb + bp) + 64 * jj], s);
+        S.t1[al][i + 64 * jj] = s;
+      }
+      __syncthreads();
+      // A2: T2_al[(b,a'), ep] = sum_c' T1_al[(b,a'), c'] conj(G[ep,al,c'])
+      for (int e = tid; e < 2 * ra * ga; e += NT) {
+        const int al = e / (ra * ga), o = e % (ra * ga), i = o % ra, ep = o / ra;
+        cplx s = czero();
+        for (int cp = 0; cp < gb; ++cp) s = cfma_bc(S.t1[al][i + 64 * cp], G[ep + ga * al + 2 * ga * cp], s);
+        S.t2[al][i + 64 * ep] = s;
+      }
+      __syncthreads();
+      // B1: T3_al[(a,a'), ep] = sum_b F[a,al,b] T2_al[(b,a'), ep]   (into t1)
+      for (int e = tid; e < 2 * rzo * ga; e += NT) {
+        const int al = e / (rzo * ga), o = e % (rzo * ga), i = o % rzo, ep = o / rzo;
+        const int aa = i / ga, ap = i % ga;
+        cplx s = czero();
+        for (int b = 0; b < fb; ++b) s = cfma(F[aa + fa * al + 2 * fa * b], S.t2[al][(b * ga + ap) + 64 * ep], s);
+        S.t1[al][i + 64 * ep] = s;
+      }
+      __syncthreads();
+      // B2 partial: P_r[i, (e, ep)] = sum_al T3_al[i, ep] conj(F[e, al, r])
+      for (int o = tid; o < rzo * fa * ga; o += NT) {
+        const int i = o % rzo, jc = o / rzo, ee = jc / ga, ep = jc % ga;
+        cplx s = czero();
+        for (int al = 0; al < 2; ++al) s = cfma_bc(S.t1[al][i + 64 * ep], F[ee + fa * al + 2 * fa * r], s);
+        S.part[i + 64 * jc] = s;
+      }
+    }
+    cl.sync();
+    // B2 sum over the F index k (CTA k's partial), column group r of GR_{c-1}
+    if (r < fa) {
+      cplx* slot = p.gr + (size_t)(c - 1) * GR_HR;
+      for (int o = tid; o < rzo * ga; o += NT) {
+        const int i = o % rzo, ep = o / rzo, jc = r * ga + ep;
+        cplx s = czero();
+        for (int k = 0; k < fb; ++k) {
+          const cplx* pk = cl.map_shared_rank(S.part, k);
+          s = cadd(s, pk[i + 64 * jc]);
+        }
+        S.grs[i + 64 * ep] = s;
+        slot[i + rzo * jc] = s;
+      }
+    }
+    cl.sync();
+  }
+}
+
+cudaError_t setup_hr_big_kernels() {
+  cudaError_t e = cudaFuncSetAttribute(k_hrb_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HrbSolveSmem));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_hr_gr_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GrClSmem));
+}
+
+cudaError_t launch_hr_gr_chain_cluster(const HrBigProb* probs_dev, int nprob, int d, cudaStream_t st) {
+  k_hr_gr_cluster<<<dim3(CLR, nprob), NT, sizeof(GrClSmem), st>>>(probs_dev, d);
+  count_launches(1);
+  return cudaGetLastError();
 }
 
 // The right-Gram chain alone for the one-CTA rounding (Kronecker ranks <= 64):

@@ -166,6 +166,8 @@ cudaError_t launch_hadamard_round_big(const HrBigProb* probs_dev, int nprob, con
 // right-Gram chain of Z = F (.) G into GR_HR slots (p.gr) for k_hadamard_round
 // (HrParams::gr_ready = 1); uses f/g cores, ranks, gr, t1, t2, t3 of HrBigProb
 cudaError_t launch_hr_gr_chain(const HrBigProb* probs_dev, int nprob, int d, cudaStream_t st);
+// the same chain for ranks <= 8 (rz <= 64) as one launch of 8-CTA clusters
+cudaError_t launch_hr_gr_chain_cluster(const HrBigProb* probs_dev, int nprob, int d, cudaStream_t st);
 
 // -------------------------------------------------------------- expansion
 struct ExProb {
