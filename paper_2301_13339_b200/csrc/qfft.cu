@@ -260,8 +260,47 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         __syncthreads();
       }
       XT_MARK(1)
-      if (w16) eig_values<16, NT>(E16, rows);
-      else eig_values<R2, NT>(S.E, rows);
+      // While warps 0 / 1 tridiagonalise (width 16), warps 2-7 form
+      // MD = M x doubled(core c+1) (rows x 4 b1, column oc = be + 2 j' as
+      // in the E layout; the last core: rows x 2), so after U only
+      // E_next = U^H MD remains (one product instead of U^H M, then x D)
+      const int a1n = S.r[c];
+      const int b1n = (c + 1 < d) ? S.r[c + 1] : 0;
+      const int mdc = (c + 1 < d) ? 4 * b1n : 2;
+      cplx* MD = S.D;   // free during the sweep (the right-Gram chain's scratch)
+      if (w16) {
+        const cplx* cn = core(c);
+        const cplx phq = phi_of(S, P, c + 1, a, t, 1);
+        auto side = [&] {
+          if (c + 1 < d) {
+            cgemm_dmma_warps(
+                rows, mdc, 2 * a1n,
+                [&](int i, int l) { return (i < rows && l < 2 * a1n) ? S.Eb[i + rows * l] : czero(); },
+                [&](int l, int oc) {
+                  const int be = oc & 1, jp = oc >> 1, sb = jp >= b1n, j = jp - sb * b1n;
+                  const int sl = l >= a1n, ii = l - sl * a1n;
+                  if (l >= 2 * a1n || oc >= mdc || sl != sb) return czero();
+                  const cplx v = cn[ii + a1n * be + 2 * a1n * j];
+                  return (sb && be) ? cmul(phq, v) : v;
+                },
+                [&](int i, int oc, cplx v) { if (i < rows && oc < mdc) MD[i + rows * oc] = v; }, 2, NT / 32 - 2);
+          } else {
+            cgemm_dmma_warps(
+                rows, 2, 2 * a1n,
+                [&](int i, int l) { return (i < rows && l < 2 * a1n) ? S.Eb[i + rows * l] : czero(); },
+                [&](int l, int be) {
+                  const int sl = l >= a1n, ii = l - sl * a1n;
+                  if (l >= 2 * a1n || be >= 2) return czero();
+                  const cplx v = cn[ii + a1n * be];
+                  return (sl && be) ? cmul(phq, v) : v;
+                },
+                [&](int i, int be, cplx v) { if (i < rows && be < 2) MD[i + rows * be] = v; }, 2, NT / 32 - 2);
+          }
+        };
+        eig_values<16, NT>(E16, rows, side);
+      } else {
+        eig_values<R2, NT>(S.E, rows);
+      }
       XT_MARK(2)
       // RANK (its T2 record deferred to the last warp during the vectors)
       if (tid < 32) {
@@ -282,40 +321,49 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         int i = e % rows, r = e / rows;
         core(c - 1)[i + rows * r] = U[i + ldk * r];
       }
+      if (w16) {
+        // next E = U_r^H MD  (rk x mdc: Eb[r + rk oc], the layout r + rk be + 2 rk j')
+        cgemm_dmma<NT / 32>(
+            rk, mdc, rows,
+            [&](int r, int i) { return (r < rk && i < rows) ? cconj(U[i + ldk * r]) : czero(); },
+            [&](int i, int oc) { return (i < rows && oc < mdc) ? MD[i + rows * oc] : czero(); },
+            [&](int r, int oc, cplx v) { if (r < rk && oc < mdc) S.Eb[r + rk * oc] = v; });
+      } else {
       // Sm = U_r^H M  (rk x cols); DMMA tiles
-      cgemm_dmma<NT / 32>(
-          rk, cols, rows,
-          [&](int r, int i) { return (r < rk && i < rows) ? cconj(U[i + ldk * r]) : czero(); },
-          [&](int i, int l) { return (i < rows && l < cols) ? S.Eb[i + rows * l] : czero(); },
-          [&](int r, int l, cplx v) { if (r < rk && l < cols) S.Sm[r + rk * l] = v; });
-      __syncthreads();
-      // next E = Sm * doubled(core c+1)
-      {
-        const int q = c + 1;
-        const int a1 = S.r[c];
-        const cplx* cn = core(q - 1);
-        if (q < d) {
-          const int b1 = S.r[q];
-          for (int e = tid; e < rk * 2 * 2 * b1; e += NT) {
-            int r = e % rk, be = (e / rk) & 1, j = e / (2 * rk);
-            cplx s;
-            if (j < b1) {
-              s = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * i], cn[i + a1 * be + 2 * a1 * j], acc); });
-            } else {
-              s = dotu<RS>(a1, [&](int i, cplx acc) {
-                return cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be + 2 * a1 * (j - b1)], acc);
-              });
-              if (be) s = cmul(phi_of(S, P, q, a, t, 1), s);
+        cgemm_dmma<NT / 32>(
+            rk, cols, rows,
+            [&](int r, int i) { return (r < rk && i < rows) ? cconj(U[i + ldk * r]) : czero(); },
+            [&](int i, int l) { return (i < rows && l < cols) ? S.Eb[i + rows * l] : czero(); },
+            [&](int r, int l, cplx v) { if (r < rk && l < cols) S.Sm[r + rk * l] = v; });
+        __syncthreads();
+        // next E = Sm * doubled(core c+1)
+        {
+          const int q = c + 1;
+          const int a1 = S.r[c];
+          const cplx* cn = core(q - 1);
+          if (q < d) {
+            const int b1 = S.r[q];
+            for (int e = tid; e < rk * 2 * 2 * b1; e += NT) {
+              int r = e % rk, be = (e / rk) & 1, j = e / (2 * rk);
+              cplx s;
+              if (j < b1) {
+                s = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * i], cn[i + a1 * be + 2 * a1 * j], acc); });
+              } else {
+                s = dotu<RS>(a1, [&](int i, cplx acc) {
+                  return cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be + 2 * a1 * (j - b1)], acc);
+                });
+                if (be) s = cmul(phi_of(S, P, q, a, t, 1), s);
+              }
+              S.Eb[e] = s;
             }
-            S.Eb[e] = s;
-          }
-        } else {
-          for (int e = tid; e < rk * 2; e += NT) {
-            int r = e % rk, be = e / rk;
-            const cplx s0 = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * i], cn[i + a1 * be], acc); });
-            cplx s1 = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be], acc); });
-            if (be) s1 = cmul(phi_of(S, P, q, a, t, 1), s1);
-            S.Eb[e] = cadd(s0, s1);
+          } else {
+            for (int e = tid; e < rk * 2; e += NT) {
+              int r = e % rk, be = e / rk;
+              const cplx s0 = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * i], cn[i + a1 * be], acc); });
+              cplx s1 = dotu<RS>(a1, [&](int i, cplx acc) { return cfma(S.Sm[r + rk * (a1 + i)], cn[i + a1 * be], acc); });
+              if (be) s1 = cmul(phi_of(S, P, q, a, t, 1), s1);
+              S.Eb[e] = cadd(s0, s1);
+            }
           }
         }
       }

@@ -142,6 +142,32 @@ __device__ __forceinline__ void cgemm_dmma(int M, int N, int K, FA fa, FB fb, FC
   }
 }
 
+// cgemm_dmma on the warps w0 .. w0 + nw - 1 only (the other warps return at
+// once; no barrier inside)
+template <class FA, class FB, class FC>
+__device__ __forceinline__ void cgemm_dmma_warps(int M, int N, int K, FA fa, FB fb, FC fc, int w0, int nw) {
+  const int lane = threadIdx.x & 31, w = (int)(threadIdx.x >> 5) - w0;
+  if (w < 0 || w >= nw) return;
+  const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, nk = (K + 3) >> 2;
+  const int ar = lane >> 2, ac = lane & 3;
+  for (int t = w; t < tm * tn; t += nw) {
+    const int ti = t % tm, tj = t / tm;
+    double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int k = 4 * kc + ac;
+      const cplx a = fa(8 * ti + ar, k);
+      const cplx b = fb(k, 8 * tj + ar);
+      dmma884(r0, r1, a.x, b.x);
+      dmma884(r0, r1, -a.y, b.y);
+      dmma884(i0, i1, a.x, b.y);
+      dmma884(i0, i1, a.y, b.x);
+    }
+    const int ci = 8 * ti + ar, cj = 8 * tj + 2 * ac;
+    fc(ci, cj, cmk(r0, i0));
+    fc(ci, cj + 1, cmk(r1, i1));
+  }
+}
+
 // ---------------------------------------------------------- cp.async
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -378,8 +404,15 @@ __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const doubl
 // REAL: the matrix is real symmetric (TT-SVD Grams) — the real one-warp path
 // for NMAX <= 20; a compile-time choice, so a complex solver carries none of
 // the real path's code and vice versa
-template <int NMAX, int NT, bool REAL = false>
-__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm) {
+struct NoSide {
+  __device__ void operator()() const {}
+};
+// side(): work of the caller run by warps 2.. while warps 0 / 1 reduce the
+// matrix (n <= 16 path only; it must not touch A0, Qm or S; warps 2.. may
+// synchronise among themselves with named barrier 3, NT - 64 threads)
+template <int NMAX, int NT, bool REAL = false, class Side = NoSide>
+__device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double* lam_out, cplx* Qm,
+                            Side side = Side()) {
   constexpr int LD = NMAX + 1;
   const int tid = threadIdx.x, lane = tid & 31;
   double anrm = 0.0;
@@ -607,6 +640,8 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
         for (int t = 0; t < 8; ++t)
           if (2 * t + h < n) Qm[i + LD * (2 * t + h)] = q[t];
       }
+    } else {
+      side();
     }
   } else {
   constexpr bool done = REAL && NMAX <= 20;
@@ -1645,13 +1680,14 @@ __device__ __noinline__ const cplx* jacobi_eig(EigSmem<NMAX>& E, int n, int* sta
 //                                eigenvalues (column-major, ld NMAX+1).
 // Tridiagonal solver first; Jacobi (whole problem again) if it reports a
 // dependent cluster (status bit ST_FALLBACK).
-template <int NMAX, int NT, bool REAL = false>
-__device__ void eig_values(EigSmem<NMAX>& E, int n) {
+template <int NMAX, int NT, bool REAL = false, class Side = NoSide>
+__device__ void eig_values(EigSmem<NMAX>& E, int n, Side side = Side()) {
   constexpr int LD = NMAX + 1;
   if constexpr (NMAX <= 16) {
     // single-warp path: E.A[0] is read, not modified (padding handled in
-    // registers), so it needs no copy for the fallback
-    trid_values<NMAX, NT>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1]);
+    // registers), so it needs no copy for the fallback; side() runs on
+    // warps 2.. meanwhile
+    trid_values<NMAX, NT, false, Side>(E.u.tr, E.A[0], LD, n, E.lam, E.V[1], side);
     return;
   }
   for (int e = threadIdx.x; e < NMAX * NMAX; e += NT) {
