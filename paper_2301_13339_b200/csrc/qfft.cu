@@ -272,8 +272,12 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         const cplx* cn = core(c);
         const cplx phq = phi_of(S, P, c + 1, a, t, 1);
         auto side = [&] {
+          // warps 2, 3, 6, 7 (sub-partitions 2 and 3): the tridiagonalising
+          // warps 0 / 1 keep sub-partitions 0 / 1 to themselves
+          const int wq = tid >> 5;
+          const int sidew = (wq == 2 || wq == 3) ? wq - 2 : ((wq == 6 || wq == 7) ? wq - 4 : -1);
           if (c + 1 < d) {
-            cgemm_dmma_warps(
+            cgemm_dmma_wl(
                 rows, mdc, 2 * a1n,
                 [&](int i, int l) { return (i < rows && l < 2 * a1n) ? S.Eb[i + rows * l] : czero(); },
                 [&](int l, int oc) {
@@ -283,9 +287,9 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
                   const cplx v = cn[ii + a1n * be + 2 * a1n * j];
                   return (sb && be) ? cmul(phq, v) : v;
                 },
-                [&](int i, int oc, cplx v) { if (i < rows && oc < mdc) MD[i + rows * oc] = v; }, 2, NT / 32 - 2);
+                [&](int i, int oc, cplx v) { if (i < rows && oc < mdc) MD[i + rows * oc] = v; }, sidew, 4);
           } else {
-            cgemm_dmma_warps(
+            cgemm_dmma_wl(
                 rows, 2, 2 * a1n,
                 [&](int i, int l) { return (i < rows && l < 2 * a1n) ? S.Eb[i + rows * l] : czero(); },
                 [&](int l, int be) {
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
                   const cplx v = cn[ii + a1n * be];
                   return (sl && be) ? cmul(phq, v) : v;
                 },
-                [&](int i, int be, cplx v) { if (i < rows && be < 2) MD[i + rows * be] = v; }, 2, NT / 32 - 2);
+                [&](int i, int be, cplx v) { if (i < rows && be < 2) MD[i + rows * be] = v; }, sidew, 4);
           }
         };
         eig_values<16, NT>(E16, rows, side);

@@ -144,9 +144,10 @@ __device__ __forceinline__ void cgemm_dmma(int M, int N, int K, FA fa, FB fb, FC
 
 // cgemm_dmma on the warps w0 .. w0 + nw - 1 only (the other warps return at
 // once; no barrier inside)
+// (wl: this warp's index among the nw participating warps, or < 0)
 template <class FA, class FB, class FC>
-__device__ __forceinline__ void cgemm_dmma_warps(int M, int N, int K, FA fa, FB fb, FC fc, int w0, int nw) {
-  const int lane = threadIdx.x & 31, w = (int)(threadIdx.x >> 5) - w0;
+__device__ __forceinline__ void cgemm_dmma_wl(int M, int N, int K, FA fa, FB fb, FC fc, int wl, int nw) {
+  const int lane = threadIdx.x & 31, w = wl;
   if (w < 0 || w >= nw) return;
   const int tm = (M + 7) >> 3, tn = (N + 7) >> 3, nk = (K + 3) >> 2;
   const int ar = lane >> 2, ac = lane & 3;
@@ -166,6 +167,11 @@ __device__ __forceinline__ void cgemm_dmma_warps(int M, int N, int K, FA fa, FB 
     fc(ci, cj, cmk(r0, i0));
     fc(ci, cj + 1, cmk(r1, i1));
   }
+}
+
+template <class FA, class FB, class FC>
+__device__ __forceinline__ void cgemm_dmma_warps(int M, int N, int K, FA fa, FB fb, FC fc, int w0, int nw) {
+  cgemm_dmma_wl(M, N, K, fa, fb, fc, (int)(threadIdx.x >> 5) - w0, nw);
 }
 
 // ---------------------------------------------------------- cp.async
