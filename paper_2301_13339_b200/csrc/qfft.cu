@@ -225,11 +225,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       // T = M G  (rows x cols), M = Eb (ld rows); DMMA tiles
       {
         const cplx* Gm = S.G[gb];
-        cgemm_dmma<NT / 32>(
-            rows, cols, cols,
-            [&](int i, int l) { return (i < rows && l < cols) ? S.Eb[i + rows * l] : czero(); },
-            [&](int l, int j) { return (l < cols && j < cols) ? Gm[l + cols * j] : czero(); },
-            [&](int i, int j, cplx v) { if (i < rows && j < cols) S.T[i + rows * j] = v; });
+        cgemm_dmma_sg<NT / 32>(GemmArgs{S.Eb, Gm, S.T, rows, cols, cols, 1, rows, 1, cols, 1, rows, 0, 0});
       }
       __syncthreads();
       if (c + 1 <= d - 1) {
@@ -246,11 +242,7 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       cplx* Kb = w16 ? E16.A[0] : S.E.A[0];
       const int ldk = w16 ? EigSmem<16>::LD : LD;
       // K = T M^H (rows x rows); DMMA tiles
-      cgemm_dmma<NT / 32>(
-          rows, rows, cols,
-          [&](int i, int l) { return (i < rows && l < cols) ? S.T[i + rows * l] : czero(); },
-          [&](int l, int j) { return (l < cols && j < rows) ? cconj(S.Eb[j + rows * l]) : czero(); },
-          [&](int i, int j, cplx v) { if (i < rows && j < rows) Kb[i + ldk * j] = v; });
+      cgemm_dmma_sg<NT / 32>(GemmArgs{S.T, S.Eb, Kb, rows, rows, cols, 1, rows, rows, 1, 1, ldk, 0, 1});
       __syncthreads();
       if (c == p) {
         double tr = 0.0;
@@ -327,18 +319,10 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       }
       if (w16) {
         // next E = U_r^H MD  (rk x mdc: Eb[r + rk oc], the layout r + rk be + 2 rk j')
-        cgemm_dmma<NT / 32>(
-            rk, mdc, rows,
-            [&](int r, int i) { return (r < rk && i < rows) ? cconj(U[i + ldk * r]) : czero(); },
-            [&](int i, int oc) { return (i < rows && oc < mdc) ? MD[i + rows * oc] : czero(); },
-            [&](int r, int oc, cplx v) { if (r < rk && oc < mdc) S.Eb[r + rk * oc] = v; });
+        cgemm_dmma_sg<NT / 32>(GemmArgs{U, MD, S.Eb, rk, mdc, rows, ldk, 1, 1, rows, 1, rk, 1, 0});
       } else {
       // Sm = U_r^H M  (rk x cols); DMMA tiles
-        cgemm_dmma<NT / 32>(
-            rk, cols, rows,
-            [&](int r, int i) { return (r < rk && i < rows) ? cconj(U[i + ldk * r]) : czero(); },
-            [&](int i, int l) { return (i < rows && l < cols) ? S.Eb[i + rows * l] : czero(); },
-            [&](int r, int l, cplx v) { if (r < rk && l < cols) S.Sm[r + rk * l] = v; });
+        cgemm_dmma_sg<NT / 32>(GemmArgs{U, S.Eb, S.Sm, rk, cols, rows, ldk, 1, 1, rows, 1, rk, 1, 0});
         __syncthreads();
         // next E = Sm * doubled(core c+1)
         {

@@ -142,6 +142,46 @@ __device__ __forceinline__ void cgemm_dmma(int M, int N, int K, FA fa, FB fb, FC
   }
 }
 
+// Strided, non-inlined form of cgemm_dmma for the per-cut products of the
+// chain kernels: one copy of the code serves every call site, so after the
+// first product of a cut it is instruction-cache resident (the inlined
+// lambda forms are separate code per site, fetched from L2 each cut).
+// C[i sc_r + j sc_c] = sum_k op(A)[i, k] op(B)[k, j], op = optional conj,
+// A[i, k] at A[i sa_r + k sa_c], B[k, j] at B[k sb_r + j sb_c].
+struct GemmArgs {
+  const cplx* A;
+  const cplx* B;
+  cplx* C;
+  int M, N, K;
+  int sa_r, sa_c, sb_r, sb_c, sc_r, sc_c;
+  int ca, cb;      // conjugate A / B
+};
+template <int NWARPS>
+__device__ __noinline__ void cgemm_dmma_sg(const GemmArgs g) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int tm = (g.M + 7) >> 3, tn = (g.N + 7) >> 3, nk = (g.K + 3) >> 2;
+  const int ar = lane >> 2, ac = lane & 3;
+  for (int t = w; t < tm * tn; t += NWARPS) {
+    const int ti = t % tm, tj = t / tm;
+    const int ri = 8 * ti + ar, cj = 8 * tj + ar;
+    double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int k = 4 * kc + ac;
+      cplx a = (ri < g.M && k < g.K) ? g.A[ri * g.sa_r + k * g.sa_c] : czero();
+      cplx b = (k < g.K && cj < g.N) ? g.B[k * g.sb_r + cj * g.sb_c] : czero();
+      if (g.ca) a.y = -a.y;
+      if (g.cb) b.y = -b.y;
+      dmma884(r0, r1, a.x, b.x);
+      dmma884(r0, r1, -a.y, b.y);
+      dmma884(i0, i1, a.x, b.y);
+      dmma884(i0, i1, a.y, b.x);
+    }
+    const int ci = 8 * ti + ar, cjo = 8 * tj + 2 * ac;
+    if (ci < g.M && cjo < g.N) g.C[ci * g.sc_r + cjo * g.sc_c] = cmk(r0, i0);
+    if (ci < g.M && cjo + 1 < g.N) g.C[ci * g.sc_r + (cjo + 1) * g.sc_c] = cmk(r1, i1);
+  }
+}
+
 // cgemm_dmma on the warps w0 .. w0 + nw - 1 only (the other warps return at
 // once; no barrier inside)
 // (wl: this warp's index among the nw participating warps, or < 0)
