@@ -177,11 +177,7 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
     // T = E GR (rows x rz, k = rz <= 64) and K = T E^H (rows x rows, k = rz)
     // on DMMA tiles (16 warps: one 8 x 8 tile of T each; the 4 tiles of K
     // with their k-chunks split over the warps and summed in a fixed order)
-    cgemm_dmma<NT / 32>(
-        rows, rz, rz,
-        [&](int i, int l) { return (i < rows && l < rz) ? S.Eb[i + rows * l] : czero(); },
-        [&](int l, int j) { return (l < rz && j < rz) ? S.Y[l + rz * j] : czero(); },
-        [&](int i, int j, cplx v) { if (i < rows && j < rz) S.Y2[i + rows * j] = v; });
+    cgemm_dmma_sg<NT / 32>(GemmArgs{S.Eb, S.Y, S.Y2, rows, rz, rz, 1, rows, 1, rz, 1, rows, 0, 0});
     __syncthreads();
     {
       // K: tile t = w & 3 (2 x 2 tiles of 8 at rows <= 16), k-split ks = w >> 2
@@ -236,12 +232,8 @@ __global__ void __launch_bounds__(NT) k_hadamard_round(const HrProb* probs, HrPa
       int i = e % rows, r = e / rows;
       oc[i + rows * r] = U[i + LD * r];
     }
-    for (int e = tid; e < rk * rz; e += NT) {
-      int r = e % rk, l = e / rk;
-      cplx s = czero();
-      for (int i = 0; i < rows; ++i) s = cfmac(U[i + LD * r], S.Eb[i + rows * l], s);
-      S.Sm[e] = s;
-    }
+    // Sm = U_r^H E (rk x rz) on DMMA tiles
+    cgemm_dmma_sg<NT / 32>(GemmArgs{U, S.Eb, S.Sm, rk, rz, rows, LD, 1, 1, rows, 1, rk, 1, 0});
     HT_MARK(3)
     // next core's F and G
     const int q = c + 1;
