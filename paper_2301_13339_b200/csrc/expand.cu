@@ -116,12 +116,42 @@ static constexpr int RSLD = NCOL + 4;        // ld of Rs rows (columns + pad)
 // R: rank capacity of the tensor (8 for the convolution output, Rhat <= 8;
 // 16 otherwise): fragments, tree and stack are sized by it, so the R = 8
 // variant keeps 3 CTAs per SM
+// Output stage variant (A/B, profiles/r02r_expand_bulk_ab.json: the bulk
+// copies lose, C4 1.10 ms against 0.59 ms, so the product build keeps the
+// streaming stores; a ring of 3-6 stage buffers leaves one CTA per SM and
+// takes 1.75 ms): with
+// -DQTT_EXPAND_BULK the interleaved R <= 8 path leaves each 2048-index block
+// as 32 rows of 512 bytes written by cp.async.bulk (shared -> global, one
+// copy per lane of warp 0) instead of 16-byte streaming stores by every
+// thread.  Stage row y sits at 640 y + 32 (y & 1) + 64 ((y >> 4) & 1) bytes:
+// linear inside the row (the copy's source), and the fragment stores of a
+// warp (lanes over x0, x1, y0, y4, x5) cover 16 distinct 8-byte bank pairs
+// per half-warp.
+#ifdef QTT_EXPAND_BULK
+static constexpr bool EX_BULK = true;
+#else
+static constexpr bool EX_BULK = false;
+#endif
+__device__ __forceinline__ int stage_pos_bulk(int q) {
+  const int x = (int)compact_even((uint64_t)q), y = (int)compact_even((uint64_t)q >> 1);
+  return y * 80 + 4 * (y & 1) + 8 * ((y >> 4) & 1) + x;
+}
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"((unsigned)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 template <int R>
 struct ExSmem {
   double Rs[2 * R * RSLD];    // [Re R; Im R] (KL x 128), row-major, ld RSLD
   cplx stack[MAXD + 2 - TOP0][R];   // stack[k - TOP0] = C_{k+1} ... C_d (size r_k), k >= TOP0 - 1
   cplx top0c[R <= 8 ? 2 * R * R : 1];  // core TOP0 (its bit flips every super-chunk), R <= 8
-  cplx tree[2][NCOL * R];     // mid tree (R > 8); the 2 x 2048-double output stage
+  cplx tree[2][NCOL * R + (EX_BULK && R <= 8 ? 256 : 0)];   // mid tree (R > 8); the 2 x 2048-double output stage
+                              // (bulk-store rows: 32 x 640 bytes)
   // R <= 8: the 7 mid cores as three products computed once per CTA,
   // P_low[b9 b10 b11] = C_9 C_10 C_11, Q_a[b12 b13] = C_12 C_13 and
   // Q_b[b14 b15] = C_14 C_15 (column (b9..b15) of R = P_low Q_a Q_b s)
@@ -225,13 +255,17 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
     for (int e = tid; e < (kl - 2 * r8) * NCOL; e += NT) S.Rs[(2 * r8 + e / NCOL) * RSLD + e % NCOL] = 0.0;
   }
   const bool il = P.layout == LAYOUT_INTERLEAVED;
+  const bool al16 = ((uintptr_t)pr.y & 15) == 0;   // else two 8-byte stores per pair
+  const bool bulk = EX_BULK && R <= 8 && il && al16;
   int spos[4][2];
 #pragma unroll
   for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) spos[mb][e] = stage_pos(32 * w + 8 * mb + (lane >> 2) + 256 * (2 * (lane & 3) + e), il);
+    for (int e = 0; e < 2; ++e) {
+      const int q = 32 * w + 8 * mb + (lane >> 2) + 256 * (2 * (lane & 3) + e);
+      spos[mb][e] = bulk ? stage_pos_bulk(q) : stage_pos(q, il);
+    }
   const uint64_t W = il ? (1ull << P.bx) : 0;
-  const bool al16 = ((uintptr_t)pr.y & 15) == 0;   // else two 8-byte stores per pair
   uint64_t prev = ~0ull;
   for (uint64_t c = c0; c < c1; ++c) {
     // ---- suffix stack over the top cores TOP0..d for the bits of c
@@ -364,6 +398,20 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       for (int mb = 0; mb < 4; ++mb)
 #pragma unroll
         for (int e = 0; e < 2; ++e) stg[spos[mb][e]] = acc[mb][e];
+      if (bulk) {
+        // the stage is read by the async proxy: order the fragment stores
+        // before it; warp 0 first makes sure the copies of the block before
+        // (the other buffer, rewritten after this barrier) have read it
+        fence_async_smem();
+        if (w == 0) bulk_wait_read0();
+        __syncthreads();
+        if (w == 0) {
+          double* yb = pr.y + qtt_offset(qbase + ((uint64_t)nb << 11), P.layout, P.bx);
+          bulk_s2g(yb + (uint64_t)lane * W, stg + lane * 80 + 4 * (lane & 1) + 8 * ((lane >> 4) & 1), 512u);
+          bulk_commit();
+        }
+        continue;
+      }
       __syncthreads();
       double* yb = pr.y + qtt_offset(qbase + ((uint64_t)nb << 11), P.layout, P.bx);
 #pragma unroll
@@ -385,6 +433,8 @@ __global__ void __launch_bounds__(NT, R <= 8 ? 3 : 2) k_expand_main(const ExProb
       }
     }
   }
+  // the stage must outlive the copies that read it
+  if (bulk && w == 0) bulk_wait_read0();
 }
 
 // ------------------------------------------------------- shard tail fold
