@@ -140,8 +140,9 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         {
           const int n2 = 2 * rc;
           cplx* g = pr.gr + (size_t)cq * GRS;
+          const bool p16 = n2 == 16;   // steady state: shifts instead of runtime divisions
           for (int e = tid; e < n2 * n2; e += NT) {
-            const int i = e % n2, j = e / n2;
+            const int i = p16 ? (e & 15) : e % n2, j = p16 ? (e >> 4) : e / n2;
             const int bi = i >= rc, bj = j >= rc, ii = i - bi * rc, jj = j - bj * rc;
             cplx v;
             if (bi == bj) v = cur[0][ii + rc * jj];
@@ -159,17 +160,17 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
         const cplx phq = phi_of(S, P, q, a, t, 1);
         cplx* TG = S.D;                       // [w][be]: a1 x rc, ld a1
         const int tsz = a1 * rc;
-        for (int e = tid; e < 4 * tsz; e += NT) {
-          const int wb = e / tsz, ij = e % tsz, i = ij % a1, j = ij / a1;
+        // element (wb, i, j) of the step's two product rounds; ranks <= 8
+        // (the steady state) map threads by shifts: the runtime divisions of
+        // the general loops cost ~100 cycles each at the head of a round
+        auto tg_elem = [&](int wb, int i, int j) {
           const int w = wb >> 1, be = wb & 1;
           const cplx* X = cur[w];
           const cplx* Cr = cc + i + a1 * be;
-          TG[e] = dotu<RS>(rc, [&](int l, cplx acc) { return cfma(Cr[2 * a1 * l], X[l + rc * j], acc); });
-        }
-        __syncthreads();
-        XT_MARK(0)
-        for (int e = tid; e < 2 * a1 * a1; e += NT) {
-          const int w = e / (a1 * a1), ij = e % (a1 * a1), i = ij % a1, j = ij / a1;
+          TG[wb * tsz + i + a1 * j] =
+              dotu<RS>(rc, [&](int l, cplx acc) { return cfma(Cr[2 * a1 * l], X[l + rc * j], acc); });
+        };
+        auto nx_elem = [&](int w, int i, int j) {
           const cplx* T0 = TG + (2 * w) * tsz + i;
           const cplx* T1 = TG + (2 * w + 1) * tsz + i;
           const cplx* C0 = cc + j;
@@ -177,6 +178,27 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
           const cplx s0 = dotu<RS>(rc, [&](int l, cplx acc) { return cfma_bc(T0[a1 * l], C0[2 * a1 * l], acc); });
           const cplx s1 = dotu<RS>(rc, [&](int l, cplx acc) { return cfma_bc(T1[a1 * l], C1[2 * a1 * l], acc); });
           nxt[w][i + a1 * j] = w == 0 ? cadd(s0, s1) : cadd(s0, cmul(phq, s1));
+        };
+        const bool small8 = NT == 256 && a1 <= 8 && rc <= 8;
+        if (small8) {
+          const int i = tid & 7, j = (tid >> 3) & 7;
+          if (i < a1 && j < rc) tg_elem(tid >> 6, i, j);
+        } else {
+          for (int e = tid; e < 4 * tsz; e += NT) {
+            const int wb = e / tsz, ij = e % tsz;
+            tg_elem(wb, ij % a1, ij / a1);
+          }
+        }
+        __syncthreads();
+        XT_MARK(0)
+        if (small8) {
+          const int i = tid & 7, j = (tid >> 3) & 7;
+          if (tid < 128 && i < a1 && j < a1) nx_elem(tid >> 6, i, j);
+        } else {
+          for (int e = tid; e < 2 * a1 * a1; e += NT) {
+            const int w = e / (a1 * a1), ij = e % (a1 * a1);
+            nx_elem(w, ij % a1, ij / a1);
+          }
         }
         __syncthreads();
         XT_MARK(0)
@@ -313,9 +335,12 @@ __global__ void __launch_bounds__(NT, 1) k_transform(const XfProb* probs, XfPara
       const int rk = S.rk;
       XT_MARK(7)
       // new core c = U_r  (ap x 2 x rk)
-      for (int e = tid; e < rows * rk; e += NT) {
-        int i = e % rows, r = e / rows;
-        core(c - 1)[i + rows * r] = U[i + ldk * r];
+      {
+        const bool p16 = rows == 16;
+        for (int e = tid; e < rows * rk; e += NT) {
+          const int i = p16 ? (e & 15) : e % rows, r = p16 ? (e >> 4) : e / rows;
+          core(c - 1)[i + rows * r] = U[i + ldk * r];
+        }
       }
       if (w16) {
         // next E = U_r^H MD  (rk x mdc: Eb[r + rk oc], the layout r + rk be + 2 rk j')

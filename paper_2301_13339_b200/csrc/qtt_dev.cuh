@@ -162,7 +162,8 @@ __device__ __noinline__ void cgemm_dmma_sg(const GemmArgs g) {
   const int tm = (g.M + 7) >> 3, tn = (g.N + 7) >> 3, nk = (g.K + 3) >> 2;
   const int ar = lane >> 2, ac = lane & 3;
   for (int t = w; t < tm * tn; t += NWARPS) {
-    const int ti = t % tm, tj = t / tm;
+    // tm <= 4 (M <= 32): no runtime division at the head of a product
+    const int tj = tm == 1 ? t : (tm == 2 ? t >> 1 : (tm == 4 ? t >> 2 : t / tm)), ti = t - tj * tm;
     const int ri = 8 * ti + ar, cj = 8 * tj + ar;
     double r0 = 0.0, r1 = 0.0, i0 = 0.0, i1 = 0.0;
     for (int kc = 0; kc < nk; ++kc) {
