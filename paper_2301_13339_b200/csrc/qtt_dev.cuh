@@ -465,9 +465,10 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
   double anrm = 0.0;
   if constexpr (NMAX <= 16) {
     // the single-warp path normalises in registers and leaves A0 untouched
-    // (it stays the original matrix for a Jacobi fallback)
+    // (it stays the original matrix for a Jacobi fallback).  The flags are
+    // next read in trid_vectors, several barriers from here on both sides:
+    // no barrier of their own
     if (tid == 0) { S.bad = 0; S.zbad = 0u; }
-    __syncthreads();
   } else {
     // ---- normalise by ||A||_F
     double nrm2 = 0.0;
@@ -520,8 +521,12 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
         nr += cabs2(a[t]);
       }
       nr = warp_sum(nr);
-      const double an = sqrt(nr);
-      const double inv = an > 0.0 ? 1.0 / an : 1.0;
+      // 1 / ||A||_F from the MUFU seed + Newton steps (the IEEE sqrt and
+      // division are ~250 cycles at the head of every solve); the IEEE forms
+      // outside the seed's range
+      const bool fastn = nr > 1e-280 && nr < 1e280;
+      const double inv = fastn ? drsqrt_nr(nr) : (nr > 0.0 ? 1.0 / sqrt(nr) : 1.0);
+      const double an = fastn ? nr * inv : sqrt(nr);
 #pragma unroll
       for (int t = 0; t < 8; ++t) a[t] = cscale(a[t], inv);
       if (lane == 0) S.anrm = an;
@@ -1039,9 +1044,11 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
     double lo = -1.0 - 1e-14, hi = 1.0 + 1e-14;
     // threads per eigenvalue: the largest power of two <= 32 with n groups in NT
     const int gl = (n * 32 <= NT) ? 32 : (n * 16 <= NT ? 16 : 8);
-    const int k = tid / gl, j = tid % gl;
+    const int lg = gl == 32 ? 5 : (gl == 16 ? 4 : 3);
+    const int k = tid >> lg, j = tid & (gl - 1);
     const int steps = gl == 32 ? 11 : (gl == 16 ? 13 : 17);
-    const double sj = (double)(j + 1) / (double)(gl + 1);
+    // (j + 1) / (gl + 1) without the division (the points only place the brackets)
+    const double sj = (double)(j + 1) * (gl == 32 ? 1.0 / 33.0 : (gl == 16 ? 1.0 / 17.0 : 1.0 / 9.0));
     double l = lo, h = hi;
     const int base = (tid & 31) & ~(gl - 1);
     const unsigned gmask = (gl == 32) ? 0xffffffffu : (((1u << gl) - 1u) << base);
@@ -1062,14 +1069,16 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       h = (first < gl) ? xh : h;
       l = (first > 0) ? xl : l;
     }
-    if (k < n && j == 0) S.lam[k] = 0.5 * (l + h);
+    if (k < n && j == 0) {
+      const double mid = 0.5 * (l + h);
+      S.lam[k] = mid;
+      lam_out[n - 1 - k] = mid * S.anrm;      // descending, in the caller's scale
+    }
 #ifdef QTT_TRID_TIMING
     if (tid == 0) { S.tstep[4] = clock64() - tb0; }
 #endif
   }
-  __syncthreads();
   (void)anrm;
-  for (int kk = tid; kk < n; kk += NT) lam_out[kk] = S.lam[n - 1 - kk] * S.anrm;
   if (tid == 0) { long long t = clock64(); S.tph[1] = t - tt0; }
   __syncthreads();
 }
@@ -1359,8 +1368,9 @@ __device__ bool trid_vectors(TridSmem<NMAX>& S, int n, int nspec, const int* nve
   if (S.bad) return false;
   if constexpr (NMAX <= 16) {
     // ---- back-transformation u = Q (D z), one output element per thread
+    const bool n16 = n == 16;
     for (int e = tid; e < n * nvec; e += NT) {
-      const int i = e % n, t = e / n;
+      const int i = n16 ? (e & 15) : e % n, t = n16 ? (e >> 4) : e / n;
       const double* z = S.Z + LD * t;
       cplx u0 = czero(), u1 = czero();
 #pragma unroll
