@@ -448,6 +448,17 @@ __device__ __forceinline__ int sturm_count(const double (&dg)[NMAX], const doubl
 #else
 #define TRID_KLOOP _Pragma("unroll")
 #endif
+// The Q-accumulating warp's reflector loop stays rolled: that warp has slack
+// (~2.7x faster per reflector than the reducing warp), and unrolled its 14
+// bodies are a second cold instruction stream fetched at the same time as
+// the reducing warp's — the two competed for the SM's instruction fetch
+// (same-box A/B: C3 12.76 -> 11.88 ms, C2 7.85 -> 7.24 ms rolled;
+// -DQTT_QWARP_UNROLLED restores the unrolled form for comparison)
+#ifdef QTT_QWARP_UNROLLED
+#define TRID_QLOOP TRID_KLOOP
+#else
+#define TRID_QLOOP _Pragma("unroll 1")
+#endif
 // REAL: the matrix is real symmetric (TT-SVD Grams) — the real one-warp path
 // for NMAX <= 20; a compile-time choice, so a complex solver carries none of
 // the real path's code and vice versa
@@ -663,7 +674,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
       cplx q[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) q[t] = cmk((2 * t + h == i) ? 1.0 : 0.0, 0.0);
-      TRID_KLOOP
+      TRID_QLOOP
       for (int k = 0; k < 14; ++k) {
         if (k + 2 >= n) break;
         const int t0 = (k + 1) >> 1;
@@ -805,7 +816,7 @@ __device__ void trid_values(TridSmem<NMAX>& S, cplx* A0, int LDA, int n, double*
         double q[NMAX];
 #pragma unroll
         for (int j = 0; j < NMAX; ++j) q[j] = (j == i) ? 1.0 : 0.0;
-        TRID_KLOOP
+        TRID_QLOOP
         for (int k = 0; k + 2 < NMAX; ++k) {
           if (k + 2 >= n) break;
           asm volatile("bar.sync 1, 64;" ::: "memory");
